@@ -1,0 +1,162 @@
+/*
+ * nlse.h -- C ABI of libnlse_b200.so: the B200-native RK4 + CD/2SHOC time step
+ * of the cubic NLSE / Gross-Pitaevskii equation (NLSEmagic, arXiv:1203.1263).
+ *
+ *   i Psi_t + a Lap(Psi) - V(r) Psi + s |Psi|^2 Psi = 0        (NLSE) P:76-80
+ *
+ * The paper's integrators take (Psi, V, a, s, h, k, scheme, BC), "simulate a
+ * 'chunk' of time-steps ... and return the resulting solution Psi" (P:415,
+ * P:480).  This ABI splits that call into create / set_psi / step / get_psi so
+ * that Psi stays resident in HBM across chunks.
+ *
+ * Conventions for every function:
+ *   - Plain C types; no torch or CUDA types in signatures (streams are void*).
+ *   - Grid layout: x fastest, offset(i,j,k) = (k*ny + j)*nx + i;
+ *     unused dims are 1.  Complex values are interleaved (re, im) pairs.
+ *   - Host Psi buffers are always double (numpy complex128 layout).  fp32
+ *     contexts round once with round-to-nearest on input (as the paper's single
+ *     precision MEX codes cast their input) and widen exactly on output.
+ *   - All buffers passed in are caller-owned; the library copies at the call and
+ *     keeps no pointer.  The context owns all device memory it allocates.
+ *   - Return value: NLSE_OK (0) or an error status; nlse_last_error() gives a
+ *     message.  A CUDA error is sticky: the context then returns NLSE_ERR_CUDA
+ *     from every call except nlse_destroy / nlse_last_error.
+ *   - Calls are synchronous at return (the device work they enqueue has
+ *     completed), except where noted.  One context per host thread.
+ *   - There is no CPU fallback: without a CUDA device nlse_create returns
+ *     NLSE_ERR_CUDA.
+ */
+#ifndef NLSE_B200_H
+#define NLSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NLSE_ABI_VERSION 1
+
+typedef struct nlse_ctx nlse_ctx;   /* opaque */
+
+typedef enum {
+    NLSE_OK = 0,
+    NLSE_ERR_ARG = 1,       /* invalid argument (message names it) */
+    NLSE_ERR_UNSTABLE = 2,  /* k above the linear stability bound, see nlse_stability_bound */
+    NLSE_ERR_OOM = 3,       /* device allocation failed */
+    NLSE_ERR_CUDA = 4,      /* CUDA error or no device (sticky) */
+    NLSE_ERR_COMM = 5,      /* multi-GPU communication error */
+    NLSE_ERR_DIVERGED = 6   /* a non-finite Psi appeared; the first step index is in nlse_last_error */
+} nlse_status;
+
+/* Boundary conditions, section "Boundary conditions" P:303-357.
+ *   DIRICHLET: Psi_b = B fixed (BCDdef) P:310-313, dPsi_b/dt = 0 (BCDdt) P:315-318,
+ *              Laplacian form (BCDlap) P:320-323 for 2SHOC.
+ *   MSD:       |Psi_b|^2 = B fixed (BCMSDdef) P:326-329, time-derivative form (msd)
+ *              P:331-335, Laplacian form (BCMSDlap) P:336-344.                      */
+typedef enum { NLSE_BC_DIRICHLET = 0, NLSE_BC_MSD = 1 } nlse_bc;
+
+/* Laplacian: CD = 2nd-order central differences; 2SHOC = the 4th-order
+ * two-step compact scheme (2shoc1d)-(3d2shocs2) P:195-299.                          */
+typedef enum { NLSE_CD2 = 2, NLSE_2SHOC4 = 4 } nlse_order;
+
+/* Working precision of the whole run: complex float or double. */
+typedef enum { NLSE_FP32 = 4, NLSE_FP64 = 8 } nlse_precision;
+
+enum {
+    NLSE_FLAG_FORCE_DT = 1u,          /* allow k above the linear bound */
+    NLSE_FLAG_GENERIC_KERNELS = 2u    /* use the one-thread-per-point kernels everywhere
+                                         (second GPU implementation, for tests) */
+};
+
+/* Create a context for an ndim-dimensional grid of dims[0] x dims[1] x dims[2]
+ * points (nx, ny, nz; dims beyond ndim must be 1), spacing h (same in every
+ * direction), coefficients a > 0 and s.
+ *   V:  host array of prod(dims) doubles, x fastest, or NULL for V = 0 (no V
+ *       array is stored and no V bytes are moved).  Copied (rounded to the
+ *       working precision) at the call.
+ * Errors: NLSE_ERR_ARG if ndim not in {1,2,3}, an active dim < 3, an inactive
+ * dim != 1, h <= 0, a <= 0, s or V not finite, or an unknown enum;
+ * NLSE_ERR_CUDA if no CUDA device; NLSE_ERR_OOM.  *out is NULL on error. */
+nlse_status nlse_create(int ndim, const int64_t dims[3], double h, double a, double s,
+                        const double *V, nlse_bc bc, nlse_order order, nlse_precision prec,
+                        uint32_t flags, nlse_ctx **out);
+
+/* Upload Psi: host array of 2*prod(dims) doubles (re, im interleaved). */
+nlse_status nlse_set_psi(nlse_ctx *ctx, const double *psi);
+/* Download Psi into a caller-owned host array of 2*prod(dims) doubles. */
+nlse_status nlse_get_psi(nlse_ctx *ctx, double *psi_out);
+
+/* Device-side I/O (for torch-owned tensors): d_psi points to prod(dims)
+ * interleaved complex values of the WORKING precision (float2 / double2) in
+ * device memory, x fastest.  Copies device-to-device on the context stream. */
+nlse_status nlse_set_psi_device(nlse_ctx *ctx, const void *d_psi);
+nlse_status nlse_get_psi_device(nlse_ctx *ctx, void *d_psi);
+
+/* Advance Psi by nsteps classic RK4 steps of size k ((RK4) P:164-180, computed
+ * in the paper's GPU form (RK4_GPU) P:495-519: four fused stage kernels per
+ * step with the Psi_tmp / Psi_out ping-pong).  Psi stays on the device.
+ * nsteps = 0 is a no-op.  Errors: NLSE_ERR_ARG (k not finite or <= 0,
+ * nsteps < 0); NLSE_ERR_UNSTABLE if k exceeds the linear bound of
+ * nlse_stability_bound and NLSE_FLAG_FORCE_DT was not given; NLSE_ERR_DIVERGED
+ * if Psi became non-finite (checked once per step inside the last stage
+ * kernel; the state is left as computed).  Results are bitwise independent of
+ * how a run is split into nlse_step calls (chunk invariance). */
+nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
+
+/* Mass M = h^d sum |Psi|^2 and Hamiltonian
+ *   H = h^d sum_p [ a sum_axes |Psi_{p+e} - Psi_p|^2 / h^2 + V_p |Psi_p|^2 - (s/2) |Psi_p|^4 ]
+ * (forward differences over pairs inside the grid; reading R-DIAG;
+ * north_star (c)).  Accumulated in fp64 with warp-shuffle + block reductions and
+ * a fixed-order final pass (deterministic). */
+nlse_status nlse_diagnostics(nlse_ctx *ctx, double *mass, double *hamiltonian);
+
+/* Linear stability bounds (stblincd) P:363-367 / (stblin2shoc) P:368-372:
+ *   CD:    k_max = h^2 / (d sqrt(2) a);   2SHOC: k_max = (3/4) h^2 / (d sqrt(2) a)
+ * and the drivers' recommended k_rec = 0.8 k_max.  No context or device needed. */
+nlse_status nlse_stability_bound(int ndim, double a, double h, nlse_order order,
+                                 double *k_max, double *k_rec);
+
+/* Message describing the last error on ctx (or the last nlse_create failure
+ * when ctx is NULL).  Valid until the next call on the same context. */
+const char *nlse_last_error(const nlse_ctx *ctx);
+const char *nlse_status_string(nlse_status st);
+
+/* Free all device memory of the context.  NULL is allowed. */
+void nlse_destroy(nlse_ctx *ctx);
+
+/* ---------------------------------------------------------------- measurement */
+
+/* The CUDA stream (cudaStream_t) the context launches on, as void*. */
+nlse_status nlse_get_stream(nlse_ctx *ctx, void **stream);
+
+/* Per-kernel timing: when enabled, nlse_step brackets every kernel launch with
+ * CUDA events on the context stream and accumulates device time per kernel
+ * kind.  Adds one event pair per launch; off by default. */
+nlse_status nlse_set_timing(nlse_ctx *ctx, int enable);
+
+#define NLSE_MAX_KINDS 8
+typedef struct {
+    int n_kinds;
+    char name[NLSE_MAX_KINDS][48];       /* kernel kind, e.g. "stage3d_stream" */
+    double ms[NLSE_MAX_KINDS];           /* accumulated device milliseconds */
+    int64_t launches[NLSE_MAX_KINDS];    /* accumulated launch count */
+    int64_t points[NLSE_MAX_KINDS];      /* accumulated grid points processed */
+} nlse_timing;
+nlse_status nlse_get_timing(nlse_ctx *ctx, nlse_timing *out);
+nlse_status nlse_reset_timing(nlse_ctx *ctx);
+
+typedef struct {
+    int64_t points;            /* prod(dims) */
+    int64_t launches_per_step; /* kernel launches per RK4 step */
+    int64_t min_bytes_per_step;/* algorithmic HBM bytes per RK4 step, (16c + 4 r_V) * points */
+    int64_t device_bytes;      /* device memory held by the context */
+    int elem_bytes;            /* sizeof(real): 4 or 8 */
+    char variant[64];          /* kernel family used for the interior */
+} nlse_info;
+nlse_status nlse_get_info(nlse_ctx *ctx, nlse_info *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLSE_B200_H */

@@ -1,0 +1,88 @@
+// common.cuh -- shared device-side definitions for the NLSE stage kernels.
+//
+// All kernels are compiled with -fmad=false (no FMA contraction), IEEE division
+// and no FTZ, and evaluate the per-point expression graph fixed in DESIGN.md
+// §3.1 (reading R-ASSOC) term by term, so that each output is bit-identical to
+// the CPU oracle.  This file holds only CUDA-side code; nothing here is shared
+// with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nlse {
+
+enum BcKind { BC_DIRICHLET = 0, BC_MSD = 1 };
+enum OrderKind { ORDER_CD = 2, ORDER_2SHOC = 4 };
+
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <typename T> using cplx = typename Vec2<T>::type;
+
+// Componentwise helpers: each is exactly one IEEE operation per component.
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { C r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { C r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }
+template <typename C, typename T> __device__ __forceinline__ C cscale(T s, C a) { C r; r.x = s * a.x; r.y = s * a.y; return r; }
+
+template <typename C> __device__ __forceinline__ C ldg_c(const C *p) { return __ldg(p); }
+
+// Per-run constants, evaluated in double on the host from the user's doubles and
+// rounded once to T (reading R-CONST).
+template <typename T> struct Consts {
+    T ih2;    // 1/h^2                (2shoc1d) P:197
+    T c76;    // 7/6                  (2shoc1d2) P:198
+    T c112;   // 1/12
+    T c16h2;  // 1/(6 h^2)
+    T a;      // a                    (NLSE) P:78
+    T s;      // s
+    T inv_a;  // 1/a                  (BCDlap) P:322, (BCMSDlap) P:338
+    T eps2;   // MSD guard (R-MSD-GUARD)
+    T kc;     // stage coefficient: k/2 (S1, S2), k (S3), k/6 (S4)   (RK4_GPU) P:495-519
+};
+
+struct Grid {
+    int64_t nx, ny, nz;   // points per axis (unused = 1)
+    int64_t sy, sz;       // strides: sy = nx, sz = nx*ny
+    int64_t n;            // total points
+};
+
+// Stage operands (RK4_GPU) P:495-519.  stage 1: Y = Psi, out = Psi_tmp;
+// stage 2: Y = Psi_tmp, out = Psi_out; stage 3: Y = Psi_out, out = Psi_tmp;
+// stage 4: Y = Psi_tmp, out = Psi (in place; Psi is read only at the owned point).
+template <typename T> struct StageArgs {
+    const cplx<T> *Y;
+    const cplx<T> *Psi;
+    cplx<T> *K;
+    cplx<T> *out;
+    const T *V;           // nullptr => V = 0 (reading R-V0)
+    Grid g;
+    Consts<T> c;
+    int *diverged;        // stage 4: atomicMin(step index) when a non-finite value is produced
+    int step;             // absolute step index (for the divergence report)
+};
+
+// RK4 stage combine at one point, (RK4_GPU) P:495-519 / (RK4) P:164-180:
+//   S1: K = F;      out = Psi + (k/2) F
+//   S2: K = K + 2F; out = Psi + (k/2) F
+//   S3: K = K + 2F; out = Psi + k F
+//   S4:             out = Psi + (k/6)(K + F)
+template <int STAGE, typename T>
+__device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, cplx<T> F, cplx<T> psi) {
+    using C = cplx<T>;
+    const T two = T(2);
+    if (STAGE == 1) {
+        A.K[q] = F;
+        A.out[q] = cadd(psi, cscale(A.c.kc, F));
+    } else if (STAGE == 2 || STAGE == 3) {
+        C k = A.K[q];
+        A.K[q] = cadd(k, cscale(two, F));
+        A.out[q] = cadd(psi, cscale(A.c.kc, F));
+    } else {
+        C k = A.K[q];
+        C r = cadd(psi, cscale(A.c.kc, cadd(k, F)));
+        A.out[q] = r;
+        if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(A.diverged, A.step);
+    }
+}
+
+}  // namespace nlse

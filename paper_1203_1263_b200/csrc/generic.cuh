@@ -1,0 +1,230 @@
+// generic.cuh -- one-thread-per-point evaluation of F(Y) at any grid point,
+// reading the stage input straight from global memory (through L1/L2).
+//
+// It serves two roles:
+//   * the boundary path of every kernel family: F at boundary points (BC time
+//     derivative form, which needs F at the inward neighbour b', recomputed
+//     here locally instead of the paper's intra-block sync), and
+//   * a complete second GPU implementation (NLSE_FLAG_GENERIC_KERNELS), the
+//     paper's kernel structure without shared-memory tiling.
+// Expression graph: DESIGN.md §3.1 (reading R-ASSOC), term by term.
+#pragma once
+#include "common.cuh"
+
+namespace nlse {
+
+template <typename T, int DIM, int ORDER, int BC>
+struct PointEval {
+    using C = cplx<T>;
+    const C *Y;
+    const T *V;
+    Grid g;
+    Consts<T> c;
+
+    __device__ __forceinline__ C y(int64_t q) const { return ldg_c(Y + q); }
+    __device__ __forceinline__ T v(int64_t q) const { return __ldg(V + q); }
+
+    __device__ __forceinline__ int n_bnd(int64_t i, int64_t j, int64_t k) const {
+        int m = (i == 0 || i == g.nx - 1);
+        if (DIM >= 2) m += (j == 0 || j == g.ny - 1);
+        if (DIM >= 3) m += (k == 0 || k == g.nz - 1);
+        return m;
+    }
+    // Inward neighbour: one step in along every boundary axis (R-MSD-NBR).
+    __device__ __forceinline__ void inward(int64_t &i, int64_t &j, int64_t &k) const {
+        i = (i == 0) ? 1 : (i == g.nx - 1 ? g.nx - 2 : i);
+        if (DIM >= 2) j = (j == 0) ? 1 : (j == g.ny - 1 ? g.ny - 2 : j);
+        if (DIM >= 3) k = (k == 0) ? 1 : (k == g.nz - 1 ? g.nz - 2 : k);
+    }
+    __device__ __forceinline__ int64_t idx(int64_t i, int64_t j, int64_t k) const {
+        return k * g.sz + j * g.sy + i;
+    }
+
+    // 2SHOC step 1 / CD at an interior point: D = (((Px-Y2)+(Py-Y2))+(Pz-Y2))*ih2.
+    __device__ __forceinline__ C D_int(int64_t q) const {
+        C y0 = y(q);
+        C y2 = cadd(y0, y0);
+        C acc = csub(cadd(y(q - 1), y(q + 1)), y2);
+        if (DIM >= 2) acc = cadd(acc, csub(cadd(y(q - g.sy), y(q + g.sy)), y2));
+        if (DIM >= 3) acc = cadd(acc, csub(cadd(y(q - g.sz), y(q + g.sz)), y2));
+        return cscale(c.ih2, acc);
+    }
+
+    // N = s|Y|^2 - V ((nbnb1) P:341-344)
+    __device__ __forceinline__ T nlin(int64_t q, C yq) const {
+        T rho = (yq.x * yq.x) + (yq.y * yq.y);
+        T n = c.s * rho;
+        if (V) n = n - v(q);
+        return n;
+    }
+
+    // Boundary D on a face point (2SHOC), Laplacian-form BC: (BCDlap) P:320-323,
+    // (BCMSDlap) P:336-344 with b' the inward normal neighbour (R-DFACE, R-MSD-LAP).
+    __device__ __forceinline__ C D_face(int64_t i, int64_t j, int64_t k) const {
+        const int64_t q = idx(i, j, k);
+        const C yb = y(q);
+        const T nb = nlin(q, yb);
+        if (BC == BC_DIRICHLET) {
+            T t = c.inv_a * nb;
+            C r; r.x = -(t * yb.x); r.y = -(t * yb.y);
+            return r;
+        } else {
+            int64_t i1 = i, j1 = j, k1 = k;
+            inward(i1, j1, k1);
+            const int64_t q1 = idx(i1, j1, k1);
+            const C y1 = y(q1);
+            const C d1 = D_int(q1);
+            T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+            T re = T(0);
+            if (!(rho1 < c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+            T n1 = nlin(q1, y1);
+            T gg = re + ((n1 - nb) * c.inv_a);
+            return cscale(gg, yb);
+        }
+    }
+
+    // D at a point that is interior or a face point.
+    __device__ __forceinline__ C D_any(int64_t i, int64_t j, int64_t k) const {
+        if (n_bnd(i, j, k) == 0) return D_int(idx(i, j, k));
+        return D_face(i, j, k);
+    }
+
+    // L at an interior point (CD: L = D; 2SHOC step 2 otherwise).
+    __device__ __forceinline__ C L_int(int64_t i, int64_t j, int64_t k) const {
+        const int64_t q = idx(i, j, k);
+        if (ORDER == ORDER_CD) return D_int(q);
+        const C d0 = D_int(q);
+        if (DIM == 1) {
+            C dm = D_any(i - 1, j, k), dp = D_any(i + 1, j, k);
+            return csub(cscale(c.c76, d0), cscale(c.c112, cadd(dm, dp)));
+        }
+        const C y4 = cscale(T(4), y(q));
+        if (DIM == 2) {
+            C cxy = csub(cadd(cadd(y(q - 1 - g.sy), y(q + 1 - g.sy)), cadd(y(q - 1 + g.sy), y(q + 1 + g.sy))), y4);
+            C sd = cadd(cadd(D_any(i - 1, j, k), D_any(i + 1, j, k)), cadd(D_any(i, j - 1, k), D_any(i, j + 1, k)));
+            C td = csub(sd, cscale(T(12), d0));
+            return csub(cscale(c.c16h2, cxy), cscale(c.c112, td));
+        }
+        C exy = csub(cadd(cadd(y(q - 1 - g.sy), y(q + 1 - g.sy)), cadd(y(q - 1 + g.sy), y(q + 1 + g.sy))), y4);
+        C exz = csub(cadd(cadd(y(q - 1 - g.sz), y(q + 1 - g.sz)), cadd(y(q - 1 + g.sz), y(q + 1 + g.sz))), y4);
+        C eyz = csub(cadd(cadd(y(q - g.sy - g.sz), y(q + g.sy - g.sz)), cadd(y(q - g.sy + g.sz), y(q + g.sy + g.sz))), y4);
+        C e = cadd(cadd(exy, exz), eyz);
+        C sd = cadd(cadd(cadd(D_any(i - 1, j, k), D_any(i + 1, j, k)), cadd(D_any(i, j - 1, k), D_any(i, j + 1, k))),
+                    cadd(D_any(i, j, k - 1), D_any(i, j, k + 1)));
+        C td = csub(sd, cscale(T(10), d0));
+        return csub(cscale(c.c16h2, e), cscale(c.c112, td));
+    }
+
+    // Interior F, (fsplit) P:424-428.
+    __device__ __forceinline__ C F_from(int64_t q, C yq, C L) const {
+        T rho = (yq.x * yq.x) + (yq.y * yq.y);
+        T sr = c.s * rho;
+        T r = (-(c.a * L.y)) - (sr * yq.y);
+        T m = (c.a * L.x) + (sr * yq.x);
+        if (V) {
+            T vq = v(q);
+            r = r + (vq * yq.y);
+            m = m - (vq * yq.x);
+        }
+        C f; f.x = r; f.y = m;
+        return f;
+    }
+    __device__ __forceinline__ C F_int(int64_t i, int64_t j, int64_t k) const {
+        const int64_t q = idx(i, j, k);
+        return F_from(q, y(q), L_int(i, j, k));
+    }
+
+    // F at a boundary point: (BCDdt) P:315-318 / (msd) P:331-335.
+    __device__ __forceinline__ C F_bnd(int64_t i, int64_t j, int64_t k) const {
+        C f;
+        if (BC == BC_DIRICHLET) { f.x = T(0); f.y = T(0); return f; }
+        int64_t i1 = i, j1 = j, k1 = k;
+        inward(i1, j1, k1);
+        const int64_t q1 = idx(i1, j1, k1);
+        const C y1 = y(q1);
+        const C f1 = F_int(i1, j1, k1);
+        T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+        T m = T(0);
+        if (!(rho1 < c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
+        const C yb = y(idx(i, j, k));
+        f.x = -(m * yb.y);
+        f.y = m * yb.x;
+        return f;
+    }
+
+    __device__ __forceinline__ C F_any(int64_t i, int64_t j, int64_t k) const {
+        if (n_bnd(i, j, k) == 0) return F_int(i, j, k);
+        return F_bnd(i, j, k);
+    }
+};
+
+// One thread per grid point over the whole grid.
+template <typename T, int DIM, int ORDER, int BC, int STAGE>
+__global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= A.g.n) return;
+    const int64_t i = q % A.g.nx;
+    const int64_t j = (q / A.g.nx) % A.g.ny;
+    const int64_t k = q / A.g.sz;
+    PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
+    cplx<T> F = ev.F_any(i, j, k);
+    cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
+    rk_combine<STAGE, T>(A, q, F, psi);
+}
+
+// Boundary points only: a flat index over the boundary surface, mapped to (i,j,k).
+// 1D: 2 points; 2D: the 2(nx + ny) - 4 perimeter; 3D: two z faces, then for each
+// interior plane the perimeter of that plane.
+template <int DIM>
+__device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t, int64_t &i, int64_t &j, int64_t &k) {
+    if (DIM == 1) {
+        if (t >= 2) return false;
+        i = t ? g.nx - 1 : 0; j = 0; k = 0;
+        return true;
+    }
+    const int64_t per = 2 * g.nx + 2 * (g.ny - 2);    // perimeter of one xy plane
+    auto perim = [&](int64_t u, int64_t &ii, int64_t &jj) {
+        if (u < g.nx) { ii = u; jj = 0; }
+        else if (u < 2 * g.nx) { ii = u - g.nx; jj = g.ny - 1; }
+        else { int64_t v = u - 2 * g.nx; ii = (v & 1) ? g.nx - 1 : 0; jj = 1 + (v >> 1); }
+    };
+    if (DIM == 2) {
+        if (t >= per) return false;
+        perim(t, i, j); k = 0;
+        return true;
+    }
+    const int64_t face = g.nx * g.ny;
+    if (t < 2 * face) {
+        k = (t < face) ? 0 : g.nz - 1;
+        int64_t u = (t < face) ? t : t - face;
+        i = u % g.nx; j = u / g.nx;
+        return true;
+    }
+    t -= 2 * face;
+    if (t >= per * (g.nz - 2)) return false;
+    k = 1 + t / per;
+    perim(t % per, i, j);
+    return true;
+}
+
+template <int DIM>
+inline int64_t n_boundary_points(const Grid &g) {
+    if (DIM == 1) return 2;
+    const int64_t per = 2 * g.nx + 2 * (g.ny - 2);
+    if (DIM == 2) return per;
+    return 2 * g.nx * g.ny + per * (g.nz - 2);
+}
+
+template <typename T, int DIM, int ORDER, int BC, int STAGE>
+__global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t i, j, k;
+    if (!bnd_point<DIM>(A.g, t, i, j, k)) return;
+    PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
+    const int64_t q = ev.idx(i, j, k);
+    cplx<T> F = ev.F_bnd(i, j, k);
+    cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
+    rk_combine<STAGE, T>(A, q, F, psi);
+}
+
+}  // namespace nlse

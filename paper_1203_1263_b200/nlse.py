@@ -1,0 +1,199 @@
+"""Thin ctypes binding of libnlse_b200.so (include/nlse.h): argument marshalling only.
+
+Same names as the C ABI.  Every step of the path runs in the library's CUDA
+kernels; importing this module loads the library and raises if it is missing
+(there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnlse_b200.so")
+
+NLSE_OK, NLSE_ERR_ARG, NLSE_ERR_UNSTABLE, NLSE_ERR_OOM, NLSE_ERR_CUDA, NLSE_ERR_COMM, NLSE_ERR_DIVERGED = range(7)
+NLSE_BC_DIRICHLET, NLSE_BC_MSD = 0, 1
+NLSE_CD2, NLSE_2SHOC4 = 2, 4
+NLSE_FP32, NLSE_FP64 = 4, 8
+NLSE_FLAG_FORCE_DT, NLSE_FLAG_GENERIC_KERNELS = 1, 2
+NLSE_MAX_KINDS = 8
+
+BC = {"dirichlet": NLSE_BC_DIRICHLET, "msd": NLSE_BC_MSD}
+ORDER = {"cd": NLSE_CD2, "2shoc": NLSE_2SHOC4}
+PREC = {"fp32": NLSE_FP32, "fp64": NLSE_FP64}
+
+
+class NLSEError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "NLSE_OK", 1: "NLSE_ERR_ARG", 2: "NLSE_ERR_UNSTABLE", 3: "NLSE_ERR_OOM", 4: "NLSE_ERR_CUDA",
+           5: "NLSE_ERR_COMM", 6: "NLSE_ERR_DIVERGED"}
+
+
+class nlse_timing(ctypes.Structure):
+    _fields_ = [("n_kinds", ctypes.c_int), ("name", (ctypes.c_char * 48) * NLSE_MAX_KINDS),
+                ("ms", ctypes.c_double * NLSE_MAX_KINDS), ("launches", ctypes.c_int64 * NLSE_MAX_KINDS),
+                ("points", ctypes.c_int64 * NLSE_MAX_KINDS)]
+
+
+class nlse_info(ctypes.Structure):
+    _fields_ = [("points", ctypes.c_int64), ("launches_per_step", ctypes.c_int64),
+                ("min_bytes_per_step", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
+                ("elem_bytes", ctypes.c_int), ("variant", ctypes.c_char * 64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    D = ctypes.POINTER(ctypes.c_double)
+    lib.nlse_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double, ctypes.c_double,
+                                ctypes.c_double, D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
+                                ctypes.POINTER(P)]
+    lib.nlse_set_psi.argtypes = [P, D]
+    lib.nlse_get_psi.argtypes = [P, D]
+    lib.nlse_set_psi_device.argtypes = [P, P]
+    lib.nlse_get_psi_device.argtypes = [P, P]
+    lib.nlse_step.argtypes = [P, ctypes.c_double, ctypes.c_int64]
+    lib.nlse_diagnostics.argtypes = [P, D, D]
+    lib.nlse_stability_bound.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int, D, D]
+    lib.nlse_last_error.argtypes = [P]
+    lib.nlse_last_error.restype = ctypes.c_char_p
+    lib.nlse_status_string.argtypes = [ctypes.c_int]
+    lib.nlse_status_string.restype = ctypes.c_char_p
+    lib.nlse_destroy.argtypes = [P]
+    lib.nlse_destroy.restype = None
+    lib.nlse_get_stream.argtypes = [P, ctypes.POINTER(P)]
+    lib.nlse_set_timing.argtypes = [P, ctypes.c_int]
+    lib.nlse_get_timing.argtypes = [P, ctypes.POINTER(nlse_timing)]
+    lib.nlse_reset_timing.argtypes = [P]
+    lib.nlse_get_info.argtypes = [P, ctypes.POINTER(nlse_info)]
+    for f in ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device", "nlse_get_psi_device",
+              "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_get_stream", "nlse_set_timing",
+              "nlse_get_timing", "nlse_reset_timing", "nlse_get_info"):
+        getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+#: every symbol include/nlse.h declares
+EXPORTS = ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device", "nlse_get_psi_device",
+           "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_last_error", "nlse_status_string",
+           "nlse_destroy", "nlse_get_stream", "nlse_set_timing", "nlse_get_timing", "nlse_reset_timing",
+           "nlse_get_info")
+
+
+def _check(st, ctx=None):
+    if st != NLSE_OK:
+        msg = lib.nlse_last_error(ctx).decode()
+        raise NLSEError(st, msg)
+
+
+def nlse_stability_bound(ndim: int, a: float, h: float, scheme: str = "2shoc"):
+    """(k_max, k_rec): linear bounds (stblincd) P:363-367 / (stblin2shoc) P:368-372, k_rec = 0.8 k_max."""
+    km, kr = ctypes.c_double(), ctypes.c_double()
+    _check(lib.nlse_stability_bound(ndim, a, h, ORDER[scheme], ctypes.byref(km), ctypes.byref(kr)))
+    return km.value, kr.value
+
+
+class Solver:
+    """Owns one nlse_ctx.  dims = (nx,), (nx, ny) or (nx, ny, nz); numpy arrays have shape
+    reversed(dims) (x fastest)."""
+
+    def __init__(self, dims, h, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc", precision="fp64",
+                 force_dt=False, generic=False):
+        self.dims = tuple(int(d) for d in dims)
+        self.shape = tuple(reversed(self.dims))
+        self.precision = precision
+        d3 = (ctypes.c_int64 * 3)(*(list(self.dims) + [1] * (3 - len(self.dims))))
+        Vp = None
+        if V is not None:
+            self._V = np.ascontiguousarray(V, dtype=np.float64)
+            assert self._V.shape == self.shape
+            Vp = self._V.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        flags = (NLSE_FLAG_FORCE_DT if force_dt else 0) | (NLSE_FLAG_GENERIC_KERNELS if generic else 0)
+        ctx = ctypes.c_void_p()
+        st = lib.nlse_create(len(self.dims), d3, h, a, s, Vp, BC[bc], ORDER[scheme], PREC[precision], flags,
+                             ctypes.byref(ctx))
+        self._V = None
+        _check(st, None)
+        self.ctx = ctx
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.nlse_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # --- C-ABI calls, same names ---------------------------------------------------------------
+    def nlse_set_psi(self, psi):
+        buf = np.ascontiguousarray(psi, dtype=np.complex128)
+        assert buf.shape == self.shape, (buf.shape, self.shape)
+        _check(lib.nlse_set_psi(self.ctx, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), self.ctx)
+
+    def nlse_get_psi(self, out=None):
+        if out is None:
+            out = np.empty(self.shape, dtype=np.complex128)
+        assert out.dtype == np.complex128 and out.flags.c_contiguous and out.shape == self.shape
+        _check(lib.nlse_get_psi(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), self.ctx)
+        return out
+
+    def nlse_set_psi_device(self, ptr: int):
+        _check(lib.nlse_set_psi_device(self.ctx, ctypes.c_void_p(ptr)), self.ctx)
+
+    def nlse_get_psi_device(self, ptr: int):
+        _check(lib.nlse_get_psi_device(self.ctx, ctypes.c_void_p(ptr)), self.ctx)
+
+    def nlse_step(self, k: float, nsteps: int):
+        _check(lib.nlse_step(self.ctx, float(k), int(nsteps)), self.ctx)
+
+    def nlse_diagnostics(self):
+        m, h = ctypes.c_double(), ctypes.c_double()
+        _check(lib.nlse_diagnostics(self.ctx, ctypes.byref(m), ctypes.byref(h)), self.ctx)
+        return m.value, h.value
+
+    def nlse_get_stream(self) -> int:
+        p = ctypes.c_void_p()
+        _check(lib.nlse_get_stream(self.ctx, ctypes.byref(p)), self.ctx)
+        return p.value or 0
+
+    def nlse_set_timing(self, enable: bool):
+        _check(lib.nlse_set_timing(self.ctx, int(bool(enable))), self.ctx)
+
+    def nlse_reset_timing(self):
+        _check(lib.nlse_reset_timing(self.ctx), self.ctx)
+
+    def nlse_get_timing(self):
+        t = nlse_timing()
+        _check(lib.nlse_get_timing(self.ctx, ctypes.byref(t)), self.ctx)
+        return {t.name[i].value.decode(): dict(ms=t.ms[i], launches=t.launches[i], points=t.points[i])
+                for i in range(t.n_kinds)}
+
+    def nlse_get_info(self):
+        t = nlse_info()
+        _check(lib.nlse_get_info(self.ctx, ctypes.byref(t)), self.ctx)
+        return dict(points=t.points, launches_per_step=t.launches_per_step,
+                    min_bytes_per_step=t.min_bytes_per_step, device_bytes=t.device_bytes,
+                    elem_bytes=t.elem_bytes, variant=t.variant.decode())
+
+    # --- conveniences ----------------------------------------------------------------------------
+    set_psi = nlse_set_psi
+    get_psi = nlse_get_psi
+    step = nlse_step
+    diagnostics = nlse_diagnostics

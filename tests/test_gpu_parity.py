@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, element by
+element, on the same seeded inputs.  Bar: bit-identical (max ulp 0), which implies
+the north-star tolerances (rel-L2 1e-12 fp64, 1e-5 fp32)."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import assert_parity, case_input, rel_l2, run_gpu, run_oracle, ulp_diff
+from paper_1203_1263_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+# Sizes span several tiles of every kernel family plus ragged tails, yet the oracle
+# finishes each case in well under a second.
+DIMS = {1: (1029,), 2: (133, 70), 3: (70, 37, 29)}
+H = {1: 0.05, 2: 0.2, 3: 0.5}
+
+
+def _k(ndim, h, scheme):
+    kb = h * h / (ndim * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
+    return 0.5 * kb
+
+
+@pytest.mark.parametrize("generic", [False, True], ids=["fast", "generic"])
+@pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_matrix_bitwise(ndim, scheme, bc, precision, withV, generic):
+    dims = DIMS[ndim]
+    h = H[ndim]
+    psi0 = case_input(dims, seed=100 + ndim)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=200 + ndim)) if withV else None
+    k = _k(ndim, h, scheme)
+    n = 12
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    ref = run_oracle(dims, h, psi0, k, n, **kw)
+    got = run_gpu(dims, h, psi0, k, n, generic=generic, **kw)
+    assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV}")
+
+
+@pytest.mark.parametrize("dims", [(3,), (4,), (3, 3), (3, 5), (5, 3), (3, 3, 3), (4, 3, 5), (3, 7, 3), (9, 3, 4)])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+def test_degenerate_small_grids(dims, scheme, bc):
+    """The smallest legal grids (3 points per axis: one interior layer) and thin slabs."""
+    psi0 = case_input(dims, seed=5)
+    h = 0.5
+    k = _k(len(dims), h, scheme)
+    ref = run_oracle(dims, h, psi0, k, 7, s=-1.0, bc=bc, scheme=scheme)
+    got = run_gpu(dims, h, psi0, k, 7, s=-1.0, bc=bc, scheme=scheme)
+    assert_parity(got, ref, "fp64", what=f"{dims}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_chunk_invariance(precision):
+    dims = (40, 33, 21)
+    psi0 = case_input(dims, seed=9)
+    k = _k(3, 0.5, "2shoc")
+    a = run_gpu(dims, 0.5, psi0, k, 24, s=-1.0, bc="msd", precision=precision)
+    b = run_gpu(dims, 0.5, psi0, k, 24, s=-1.0, bc="msd", precision=precision, chunks=[1, 5, 7, 11])
+    assert ulp_diff(a, b, precision) == 0
+
+
+def test_config1_bright_soliton_full():
+    """configs[0]: 1D bright soliton, N=1025, h=0.05, 2SHOC fp64 Dirichlet, 1000 steps: bitwise vs the
+    oracle and within the exact-solution error."""
+    cfg = inputs.config("bright1d")
+    kw = dict(a=1.0, s=1.0, bc="dirichlet", scheme="2shoc", precision="fp64")
+    ref = run_oracle(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], cfg["steps"], **kw)
+    got = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], cfg["steps"], force_dt=False, **kw)
+    assert_parity(got, ref, "fp64", what="config 1")
+    ex = inputs.bright_soliton(inputs.axis(1025, cfg["h"]), t=1.0)
+    assert np.abs(got - ex).max() < 2e-6
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+def test_config2_dark_soliton_orders(scheme, precision):
+    """configs[1]: dark soliton, MSD, t=5 on [-50, 50]: GPU orders 2 / 4 and bitwise = oracle at h = 0.1."""
+    errs = []
+    for h in (0.2, 0.1, 0.05):
+        n = int(round(100 / h)) + 1
+        x = inputs.axis(n, h)
+        kb = h * h / math.sqrt(2) * (0.75 if scheme == "2shoc" else 1.0)
+        nst = math.ceil(5.0 / (0.8 * kb))
+        kw = dict(a=1.0, s=-1.0, bc="msd", scheme=scheme, precision=precision)
+        got = run_gpu((n,), h, inputs.dark_soliton(x), 5.0 / nst, nst, force_dt=False, **kw)
+        if h == 0.1:
+            ref = run_oracle((n,), h, inputs.dark_soliton(x), 5.0 / nst, nst, **kw)
+            assert_parity(got, ref, precision, what=f"dark soliton {scheme} {precision}")
+        errs.append(np.abs(got - inputs.dark_soliton(x, t=5.0)).max())
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    want = 2.0 if scheme == "cd" else 4.0
+    if precision == "fp64" or scheme == "cd":
+        assert all(abs(o - want) < 0.3 for o in orders), (errs, orders)
+
+
+def test_config3_trap2d_full_size():
+    """configs[2]: 2D vortex in a harmonic trap, 1024^2, 2SHOC fp64 MSD: 10 steps bitwise vs the oracle."""
+    cfg = inputs.config("trap2d")
+    kw = dict(a=1.0, s=-1.0, V=cfg["V"], bc="msd", scheme="2shoc", precision="fp64")
+    ref = run_oracle(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 10, **kw)
+    got = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 10, force_dt=False, **kw)
+    assert_parity(got, ref, "fp64", what="config 3")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_config4_ring_full_size(precision):
+    """configs[3]: 3D vortex ring 87x87x203, 2SHOC MSD: 20 steps bitwise vs the oracle."""
+    cfg = inputs.config("ring3d")
+    kw = dict(a=1.0, s=-1.0, bc="msd", scheme="2shoc", precision=precision)
+    ref = run_oracle(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 20, **kw)
+    got = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 20, force_dt=False, **kw)
+    assert_parity(got, ref, precision, what=f"config 4 {precision}")
+
+
+def test_config4_ring_3360_steps_properties():
+    """The paper's benchmark run (3360 steps): finite, MSD keeps the boundary density, and the fp32 run
+    tracks the fp64 run (the oracle would need ~15 min; properties that hold at any length instead)."""
+    cfg = inputs.config("ring3d")
+    kw = dict(a=1.0, s=-1.0, bc="msd", scheme="2shoc", force_dt=False)
+    d = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 3360, precision="fp64", **kw)
+    f = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], 3360, precision="fp32", **kw)
+    assert np.all(np.isfinite(d)) and np.all(np.isfinite(f))
+    rho0 = np.abs(cfg["psi0"]) ** 2
+    for sl in [(0, slice(None), slice(None)), (slice(None), 0, slice(None)), (slice(None), slice(None), -1)]:
+        assert np.abs(np.abs(d[sl]) ** 2 - rho0[sl]).max() < 1e-6
+    assert rel_l2(f, d) < 1e-4
+
+
+def test_diagnostics_match_oracle():
+    import oracle
+    from paper_1203_1263_b200.nlse import Solver
+    for dims, V in [((1025,), None), ((130, 77), None), ((40, 30, 20), "V")]:
+        psi = case_input(dims, seed=31)
+        Vv = np.abs(inputs.random_smooth(dims, seed=32)) if V else None
+        for prec in ("fp64", "fp32"):
+            with Solver(dims, 0.2, a=0.8, s=-1.2, V=Vv, bc="msd", precision=prec) as sv:
+                sv.nlse_set_psi(psi)
+                m, h = sv.nlse_diagnostics()
+                p = oracle.Problem(dims, 0.2, a=0.8, s=-1.2, bc="msd", precision=prec)
+                src = psi if prec == "fp64" else psi.astype(np.complex64)
+                mo, ho = oracle.diagnostics(p, src, Vv)
+                assert abs(m - mo) <= 1e-12 * abs(mo) and abs(h - ho) <= 1e-12 * abs(ho), (dims, prec, m, mo, h, ho)
+
+
+def test_errors_and_edge_cases():
+    from paper_1203_1263_b200.nlse import NLSE_ERR_ARG, NLSE_ERR_DIVERGED, NLSE_ERR_UNSTABLE, NLSEError, Solver
+    dims = (31, 17)
+    psi = case_input(dims, seed=3)
+    with Solver(dims, 0.1, s=-1.0, bc="msd") as sv:
+        sv.nlse_set_psi(psi)
+        sv.nlse_step(0.001, 0)                      # no-op
+        assert np.array_equal(sv.nlse_get_psi(), psi)
+        with pytest.raises(NLSEError) as e:
+            sv.nlse_step(0.01, 1)                   # above the 2D 2SHOC bound 0.00265
+        assert e.value.status == NLSE_ERR_UNSTABLE
+        with pytest.raises(NLSEError) as e:
+            sv.nlse_step(-0.001, 1)
+        assert e.value.status == NLSE_ERR_ARG
+        with pytest.raises(NLSEError) as e:
+            sv.nlse_step(float("nan"), 1)
+        assert e.value.status == NLSE_ERR_ARG
+    with Solver(dims, 0.1, s=-1.0, bc="dirichlet", force_dt=True) as sv:
+        sv.nlse_set_psi(psi)
+        with pytest.raises(NLSEError) as e:
+            sv.nlse_step(0.05, 400)                 # far above the bound: blows up
+        assert e.value.status == NLSE_ERR_DIVERGED
+        assert "step" in str(e.value)
+
+
+def test_device_io_roundtrip():
+    import torch
+    from paper_1203_1263_b200.nlse import Solver
+    dims = (20, 10, 6)
+    psi = case_input(dims, seed=4)
+    for prec, dt in (("fp64", torch.complex128), ("fp32", torch.complex64)):
+        with Solver(dims, 0.3, precision=prec) as sv:
+            t = torch.from_numpy(psi.astype(np.complex128 if prec == "fp64" else np.complex64)).cuda()
+            sv.nlse_set_psi_device(t.data_ptr())
+            u = torch.empty_like(t)
+            sv.nlse_get_psi_device(u.data_ptr())
+            torch.cuda.synchronize()
+            assert torch.equal(t, u)
+            assert np.array_equal(sv.nlse_get_psi(), t.cpu().numpy().astype(np.complex128))
