@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py -- grid-point RK4 updates/s of the NLSE/GPE hot path (BASELINE.json metric).
+
+Workload (N = 1): BASELINE configs[4], the 3D 1024^3 GPE, RK4 + 2SHOC, fp64, MSD,
+harmonic-trap V array (the 3D fp64 2SHOC configuration the metric is quoted on at
+1/2/4/8 GPUs; 77.3 GB of device state, far larger than L2).  A "step" is one RK4
+step of the whole grid (all §8(a) rows: 4 fused stage kernels + boundary kernels).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpe3d|gpe3d_512|ring3d|...]
+    python bench.py --impl reference ...     # the CPU oracle arm
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point RK4 updates/sec (3D 2SHOC fp64/fp32) and % HBM roofline at 1/2/4/8 GPU"
+UNIT = "grid-point RK4 updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpe3d")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--generic", action="store_true", help="use the one-thread-per-point kernels")
+    return ap.parse_args()
+
+
+def workload(name):
+    from paper_1203_1263_b200 import inputs
+    cfg = inputs.config(name)
+    if name.startswith("gpe3d"):
+        n = cfg["dims"][0]
+        psi, V = inputs.gpe3d_fill(n)
+        cfg["psi0"], cfg["V"] = psi, V
+    return cfg
+
+
+def bytes_min_per_point(cfg):
+    """B_min = 16c + 4 r_V bytes per point per RK4 step."""
+    r = 8 if cfg["precision"] == "fp64" else 4
+    return 16 * 2 * r + (4 * r if cfg["V"] is not None else 0)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic(variant):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if d.get("variant") == variant and d.get("dram_bytes_per_launch"):
+            return float(d["dram_bytes_per_launch"]), os.path.basename(f)
+    return None, None
+
+
+def cpu_baseline_sample(cfg, seconds_hint=15.0):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same workload:
+    a z-slab of the workload's initial condition (its own MSD boundary), one or more RK4 steps."""
+    import oracle
+    oracle.build()
+    nx, ny, nz = (list(cfg["dims"]) + [1, 1])[:3]
+    psi, V = cfg["psi0"], cfg["V"]
+    if len(cfg["dims"]) == 3:
+        planes = max(3, min(nz, int(2.0e6 * seconds_hint / 3.0 / (nx * ny)) or 3))
+        z0 = max(0, nz // 2 - planes // 2)
+        sub = np.ascontiguousarray(psi[z0:z0 + planes])
+        Vs = None if V is None else np.ascontiguousarray(V[z0:z0 + planes])
+        dims = (nx, ny, planes)
+        desc = f"{nx}x{ny}x{planes} z-slab (planes {z0}..{z0 + planes - 1}) of the workload IC"
+    else:
+        sub, Vs, dims = psi, V, cfg["dims"]
+        desc = "full workload grid"
+    p = oracle.Problem(dims, cfg["h"], a=cfg["a"], s=cfg["s"], bc=cfg["bc"], scheme=cfg["scheme"],
+                       precision=cfg["precision"])
+    t0 = time.perf_counter()
+    nst = 0
+    while True:
+        sub = oracle.step(p, sub, cfg["k"], 1, Vs)
+        nst += 1
+        el = time.perf_counter() - t0
+        if el > seconds_hint * 0.5 or nst >= 50:
+            break
+    pts = int(np.prod(dims))
+    return {"value": pts * nst / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{desc}, {nst} RK4 step(s), serial C oracle (-O2 -ffp-contract=off), {el:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle arm, on this arm's config/metric, each step a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    from paper_1203_1263_b200 import inputs
+    cfg = inputs.config(args.config)
+    nx, ny, nz = (list(cfg["dims"]) + [1, 1])[:3]
+    if args.config.startswith("gpe3d"):
+        planes = 4
+        z0 = nz // 2 - planes // 2
+        psi, V = inputs.gpe3d_slab(nx, z0, z0 + planes, cfg["h"])
+        dims = (nx, ny, planes)
+        desc = f"{nx}x{ny}x{planes} z-slab (planes {z0}..{z0 + planes - 1}) of the {nx}^3 workload, 1 RK4 step per bench step"
+    else:
+        psi, V, dims = cfg["psi0"], cfg["V"], cfg["dims"]
+        desc = "full workload grid, 1 RK4 step per bench step"
+    p = oracle.Problem(dims, cfg["h"], a=cfg["a"], s=cfg["s"], bc=cfg["bc"], scheme=cfg["scheme"],
+                       precision=cfg["precision"])
+    for _ in range(args.warmup):
+        psi = oracle.step(p, psi, cfg["k"], 1, V)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        psi = oracle.step(p, psi, cfg["k"], 1, V)
+    el = time.perf_counter() - t0
+    pts = int(np.prod(dims))
+    val = pts * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if cfg["precision"] == "fp64" else "f32", "data": "synthetic",
+            "config": config_block(cfg, args),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, args):
+    return {"workload": f"{cfg['name']}: {'x'.join(map(str, cfg['dims']))} {cfg['scheme'].upper()} RK4, "
+                        f"{cfg['bc'].upper()} BC, {cfg['precision']}, "
+                        f"{'harmonic-trap V array' if cfg.get('has_V', cfg['V'] is not None) else 'V=0'} (BASELINE.json configs)",
+            "grid": list(cfg["dims"]), "h": cfg["h"], "k": cfg["k"], "scheme": cfg["scheme"], "bc": cfg["bc"],
+            "precision": cfg["precision"], "a": cfg["a"], "s": cfg["s"],
+            "parallelism": f"z-slab x{args.gpus}" if args.gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2 (no flush needed)" if int(np.prod(cfg["dims"])) * 64 > 2e9
+                  else "working set L2-resident (L2-scale config, no flush)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_1203_1263_b200 import build
+    build.build()
+    from paper_1203_1263_b200.nlse import Solver
+
+    cfg = workload(args.config)
+    B = bytes_min_per_point(cfg)
+    peak, peak_src = measured_peaks()
+    npts = int(np.prod(cfg["dims"]))
+    sv = Solver(cfg["dims"], cfg["h"], a=cfg["a"], s=cfg["s"], V=cfg["V"], bc=cfg["bc"], scheme=cfg["scheme"],
+                precision=cfg["precision"], generic=args.generic)
+    info = sv.nlse_get_info()
+    sv.nlse_set_psi(cfg["psi0"])
+    stream = torch.cuda.ExternalStream(sv.nlse_get_stream())
+    k = cfg["k"]
+    sv.nlse_step(k, args.warmup)
+    sv.nlse_set_timing(True)
+    sv.nlse_reset_timing()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        sv.nlse_step(k, args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    sv.nlse_set_timing(False)
+    timing = sv.nlse_get_timing()
+    value = npts * args.steps / (ms / 1e3)
+
+    # dominant kernel: the interior stage kernel family
+    dom = info["variant"]
+    td = timing[dom]
+    avg_launch_ms = td["ms"] / max(td["launches"], 1)
+    pts_per_launch = td["points"] / max(td["launches"], 1)
+    alg_bytes_launch = pts_per_launch * B / 4.0          # B_min per point per step spread over 4 stages
+    achieved = alg_bytes_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(dom)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": dom, "alg_bytes_per_launch": alg_bytes_launch, "avg_launch_ms": avg_launch_ms,
+            "peak_source": peak_src, "traffic_source": traffic_src,
+            "kernel_share_of_step": round(td["ms"] / sum(v["ms"] for v in timing.values() if v["launches"]), 4),
+            "step_frac_of_roofline": round(value * B / 1e9 / peak, 4),
+            "bytes_per_point_step": B}
+
+    # e2e: the paper's chunk model through the public API with host buffers: per chunk of
+    # `steps` RK4 steps, H2D of Psi from pinned memory, the steps, D2H of Psi to pinned memory.
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.empty(npts * 2, dtype=torch.float64, pin_memory=True)
+        host = pinned.numpy().view(np.complex128).reshape(tuple(reversed(cfg["dims"])))
+        host[...] = cfg["psi0"]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sv.nlse_set_psi(host)
+        sv.nlse_step(k, args.steps)
+        sv.nlse_get_psi(host)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": npts * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": npts * 16 // args.steps,
+               "d2h_bytes_per_step": npts * 16 // args.steps, "chunk_steps": args.steps,
+               "what": "nlse_set_psi(pinned host) + nlse_step(k, steps) + nlse_get_psi(pinned host), wall clock"}
+        del pinned, host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(cfg)
+    sv.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64" if cfg["precision"] == "fp64" else "f32", "data": "synthetic",
+                "config": config_block(cfg, args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(args.steps * info["launches_per_step"]), "clocks": clk.summary(),
+                "kernel_timing": {k2: v for k2, v in timing.items() if v["launches"]},
+                "pct_hbm_roofline": round(100 * value * B / 1e9 / peak, 2)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -139,7 +139,8 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
         return;
     }
     {
-        LaunchTimer lt(c, c->interior_kind, c->g.n);
+        const int64_t ni = (c->g.nx - 2) * (DIM >= 2 ? c->g.ny - 2 : 1) * (DIM >= 3 ? c->g.nz - 2 : 1);
+        LaunchTimer lt(c, c->interior_kind, ni);
         if (DIM == 3) launch_stream3d<T, ORDER, BC, STAGE>(A, c->stream);
         else if (DIM == 2) launch_tile2d<T, ORDER, BC, STAGE>(A, c->stream);
         else launch_tile1d<T, ORDER, BC, STAGE>(A, c->stream);

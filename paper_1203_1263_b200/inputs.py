@@ -148,21 +148,16 @@ def config(name: str):
                     psi0=vortex_ring(dims, h, d=5.0), V=None)
     if name.startswith("gpe3d"):   # configs[4]: gpe3d (1024^3) or gpe3d_<n> for smaller cubes
         n = int(name.split("_")[1]) if "_" in name else 1024
-        dims = (n, n, n)
-        h = 0.25
-        w = 1.0 / 320.0 * (1024.0 / n)
-        V = harmonic_trap(dims, h, w)
-        d = 32.0 * n / 1024.0
-        return dict(name=name, dims=dims, h=h, k=0.005, steps=100, a=1.0, s=-1.0, bc="msd",
-                    scheme="2shoc", precision="fp64",
-                    psi0=None if n >= 512 else thomas_fermi(vortex_ring(dims, h, d=d), V),
-                    V=None if n >= 512 else V, w=w, ring_d=d)
+        return dict(name=name, dims=(n, n, n), h=0.25, k=0.005, steps=100, a=1.0, s=-1.0, bc="msd",
+                    scheme="2shoc", precision="fp64", psi0=None, V=None, has_V=True,
+                    w=1.0 / 320.0 * (1024.0 / n), ring_d=32.0 * n / 1024.0)
     raise KeyError(name)
 
 
 def gpe3d_slab(n: int, z0: int, z1: int, h: float = 0.25):
-    """Planes [z0, z1) of the n^3 GPE workload (ring x sqrt(1 - V), V = w^2 r^2), generated slab by
-    slab so that the 1024^3 input never needs two full-size float64 temporaries on the host."""
+    """Planes [z0, z1) of the n^3 GPE workload (configs[4], reading R-TRAP): a vortex ring of radius
+    d = 32 n/1024 (R-RING, c = 0.5) times the Thomas-Fermi envelope sqrt(1 - V), V = w^2 r^2 with
+    w = (1/320)(1024/n).  Returns (psi complex128, V float64), shape (z1 - z0, n, n)."""
     w = 1.0 / 320.0 * (1024.0 / n)
     d = 32.0 * n / 1024.0
     ax = axis(n, h)
@@ -177,3 +172,24 @@ def gpe3d_slab(n: int, z0: int, z1: int, h: float = 0.25):
     psi = g * np.exp(1j * (np.arctan2(Zc, rp) - np.arctan2(Zc, rm))) * np.exp(1j * 0.25 * Z)
     psi *= np.sqrt(np.clip(1.0 - V, 0.0, None))
     return psi, V
+
+
+def gpe3d_fill(n: int, psi_out=None, V_out=None, threads: int = 0, h: float = 0.25):
+    """The full n^3 GPE workload, generated slab by slab on all host cores (numpy releases the GIL)
+    into caller-provided (or new) arrays of shape (n, n, n).  Identical values to gpe3d_slab."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    if psi_out is None:
+        psi_out = np.empty((n, n, n), np.complex128)
+    if V_out is None:
+        V_out = np.empty((n, n, n), np.float64)
+    slab = max(1, min(8, n // 8))
+
+    def work(z0):
+        z1 = min(n, z0 + slab)
+        p, v = gpe3d_slab(n, z0, z1, h)
+        psi_out[z0:z1] = p
+        V_out[z0:z1] = v
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(work, range(0, n, slab)))
+    return psi_out, V_out
