@@ -228,3 +228,23 @@ __global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
 }
 
 }  // namespace nlse
+
+namespace nlse {
+
+// Interior points only, one thread per point (flat index over the interior box).
+template <typename T, int DIM, int ORDER, int BC, int STAGE>
+__global__ void __launch_bounds__(256) stage_interior_generic(StageArgs<T> A) {
+    const int64_t mx = A.g.nx - 2, my = DIM >= 2 ? A.g.ny - 2 : 1, mz = DIM >= 3 ? A.g.nz - 2 : 1;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= mx * my * mz) return;
+    const int64_t i = 1 + t % mx;
+    const int64_t j = DIM >= 2 ? 1 + (t / mx) % my : 0;
+    const int64_t k = DIM >= 3 ? 1 + t / (mx * my) : 0;
+    PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
+    const int64_t q = ev.idx(i, j, k);
+    cplx<T> F = ev.F_int(i, j, k);
+    cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
+    rk_combine<STAGE, T>(A, q, F, psi);
+}
+
+}  // namespace nlse
