@@ -44,10 +44,30 @@ def parse():
     return ap.parse_args()
 
 
-def workload(name):
+def workload(name, rank=0, world=1):
+    """The workload's initial condition (and V): the whole grid at N = 1, this rank's z slab
+    (planes [z0, z0 + nloc) of nlse_slab_range) in slab mode."""
     from paper_1203_1263_b200 import inputs
     cfg = inputs.config(name)
-    if name.startswith("gpe3d"):
+    cfg["z0"], cfg["nloc"] = 0, (cfg["dims"][2] if len(cfg["dims"]) == 3 else 1)
+    if world > 1:
+        from paper_1203_1263_b200.nlse import nlse_slab_range
+        z0, nl = nlse_slab_range(cfg["dims"][2], world, rank)
+        cfg["z0"], cfg["nloc"] = z0, nl
+        if name.startswith("gpe3d"):
+            n = cfg["dims"][0]
+            psi = np.empty((nl, n, n), np.complex128)
+            V = np.empty((nl, n, n), np.float64)
+            step = 8
+            for a in range(0, nl, step):
+                b = min(nl, a + step)
+                psi[a:b], V[a:b] = inputs.gpe3d_slab(n, z0 + a, z0 + b, cfg["h"])
+            cfg["psi0"], cfg["V"] = psi, V
+        else:
+            cfg["psi0"] = np.ascontiguousarray(cfg["psi0"][z0:z0 + nl])
+            if cfg["V"] is not None:
+                cfg["V"] = np.ascontiguousarray(cfg["V"][z0:z0 + nl])
+    elif name.startswith("gpe3d"):
         n = cfg["dims"][0]
         psi, V = inputs.gpe3d_fill(n)
         cfg["psi0"], cfg["V"] = psi, V
@@ -228,13 +248,17 @@ def main():
     build.build()
     from paper_1203_1263_b200.nlse import Solver
 
-    cfg = workload(args.config)
+    cfg = workload(args.config, rank, world)
     B = bytes_min_per_point(cfg)
     peak, peak_src = measured_peaks()
-    npts = int(np.prod(cfg["dims"]))
+    npts = int(np.prod(cfg["dims"]))              # whole job
     sv = Solver(cfg["dims"], cfg["h"], a=cfg["a"], s=cfg["s"], V=cfg["V"], bc=cfg["bc"], scheme=cfg["scheme"],
-                precision=cfg["precision"], generic=args.generic)
+                precision=cfg["precision"], generic=args.generic, dist=(rank, world) if world > 1 else None)
+    if world > 1:
+        from paper_1203_1263_b200 import dist as pdist
+        pdist.connect(sv)
     info = sv.nlse_get_info()
+    nloc_pts = info["points"]
     sv.nlse_set_psi(cfg["psi0"])
     stream = torch.cuda.ExternalStream(sv.nlse_get_stream())
     k = cfg["k"]
@@ -279,8 +303,8 @@ def main():
     # `steps` RK4 steps, H2D of Psi from pinned memory, the steps, D2H of Psi to pinned memory.
     e2e = None
     if not args.no_e2e:
-        pinned = torch.empty(npts * 2, dtype=torch.float64, pin_memory=True)
-        host = pinned.numpy().view(np.complex128).reshape(tuple(reversed(cfg["dims"])))
+        pinned = torch.empty(nloc_pts * 2, dtype=torch.float64, pin_memory=True)
+        host = pinned.numpy().view(np.complex128).reshape(sv.shape)
         host[...] = cfg["psi0"]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -294,7 +318,8 @@ def main():
             el = float(t.item())
         e2e = {"value": npts * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": npts * 16 // args.steps,
                "d2h_bytes_per_step": npts * 16 // args.steps, "chunk_steps": args.steps,
-               "what": "nlse_set_psi(pinned host) + nlse_step(k, steps) + nlse_get_psi(pinned host), wall clock"}
+               "what": "nlse_set_psi(pinned host) + nlse_step(k, steps) + nlse_get_psi(pinned host), wall clock, "
+                       "max over ranks; bytes summed over ranks (complex128 host I/O)"}
         del pinned, host
 
     cpu = None

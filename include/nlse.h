@@ -104,11 +104,55 @@ nlse_status nlse_get_psi_device(nlse_ctx *ctx, void *d_psi);
  * how a run is split into nlse_step calls (chunk invariance). */
 nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
 
+/* ---------------------------------------------------------------- slab mode (§8(e))
+ * A 3D grid partitioned into contiguous z slabs, one per rank (one GPU per process,
+ * or several "virtual ranks" in one process).  Rank r owns global planes
+ * [z0, z0 + nloc) of nlse_slab_range.  Buffers read with a halo carry w ghost planes
+ * on each side (w = 1 CD, 2 2SHOC); every stage kernel stores the outputs of its
+ * first / last w planes also into the neighbours' ghost planes over peer memory
+ * (NVLink P2P through CUDA IPC), and a device-side neighbour barrier separates the
+ * stages.  Results are bitwise identical to the single-GPU run.
+ *
+ * In slab mode nlse_set_psi*, nlse_step and nlse_diagnostics are COLLECTIVE: every
+ * rank calls them in the same order (like NCCL collectives).  Psi / V host buffers
+ * hold the local slab (nloc planes).  1D and 2D grids are not partitioned (they run as
+ * independent replicas). */
+#define NLSE_MAX_RANKS 16
+#define NLSE_DIST_HANDLE_BYTES 512
+
+/* Balanced split of nz planes over nranks: rank r gets nz/nranks planes, +1 for the
+ * first nz % nranks ranks, starting at *z0.  Host only. */
+nlse_status nlse_slab_range(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *nloc);
+
+/* Create the slab context of `rank`: dims are the GLOBAL grid (ndim must be 3); V_local
+ * is the rank's slab of V (nloc planes) or NULL.  Errors as nlse_create, plus
+ * NLSE_ERR_ARG if a slab has fewer than 2w planes or rank/nranks are out of range. */
+nlse_status nlse_create_dist(int ndim, const int64_t dims[3], double h, double a, double s,
+                             const double *V_local, nlse_bc bc, nlse_order order,
+                             nlse_precision prec, uint32_t flags, int rank, int nranks,
+                             nlse_ctx **out);
+/* Write this rank's NLSE_DIST_HANDLE_BYTES-byte handle (CUDA IPC handles of its halo'd
+ * buffers and comm block) into `handle`; the caller exchanges them (e.g. an
+ * all-gather over torch.distributed). */
+nlse_status nlse_dist_export(nlse_ctx *ctx, void *handle);
+/* Map the peers: `handles` = nranks handles in rank order (this rank's included).
+ * NLSE_ERR_COMM if a handle is malformed or cannot be opened. */
+nlse_status nlse_dist_connect(nlse_ctx *ctx, const void *handles);
+/* Virtual ranks: connect the n slab contexts of ONE process (ranks 0..n-1 in order,
+ * any devices).  Drive them with the _group calls below. */
+nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n);
+/* nlse_step / nlse_diagnostics over a group of contexts driven by one host thread
+ * (work is enqueued interleaved per stage; mass[j], hamiltonian[j] per context, all
+ * equal in slab mode). */
+nlse_status nlse_step_group(nlse_ctx *const *ctxs, int n, double k, int64_t nsteps);
+nlse_status nlse_diagnostics_group(nlse_ctx *const *ctxs, int n, double *mass, double *hamiltonian);
+
 /* Mass M = h^d sum |Psi|^2 and Hamiltonian
  *   H = h^d sum_p [ a sum_axes |Psi_{p+e} - Psi_p|^2 / h^2 + V_p |Psi_p|^2 - (s/2) |Psi_p|^4 ]
  * (forward differences over pairs inside the grid; reading R-DIAG;
  * north_star (c)).  Accumulated in fp64 with warp-shuffle + block reductions and
- * a fixed-order final pass (deterministic). */
+ * a fixed-order final pass (deterministic).  Slab mode: global sums (per-rank partials
+ * exchanged over peer memory and added in rank order; collective). */
 nlse_status nlse_diagnostics(nlse_ctx *ctx, double *mass, double *hamiltonian);
 
 /* Linear stability bounds (stblincd) P:363-367 / (stblin2shoc) P:368-372:
@@ -153,6 +197,8 @@ typedef struct {
     int64_t device_bytes;      /* device memory held by the context */
     int elem_bytes;            /* sizeof(real): 4 or 8 */
     char variant[64];          /* kernel family used for the interior */
+    int rank, nranks;          /* slab mode (0, 1 otherwise) */
+    int64_t z0, nz_local;      /* owned global planes [z0, z0 + nz_local) */
 } nlse_info;
 nlse_status nlse_get_info(nlse_ctx *ctx, nlse_info *out);
 

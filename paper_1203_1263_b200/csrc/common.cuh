@@ -40,11 +40,21 @@ template <typename T> struct Consts {
     T kc;     // stage coefficient: k/2 (S1, S2), k (S3), k/6 (S4)   (RK4_GPU) P:495-519
 };
 
+// The grid a context owns.  Single GPU: the whole grid.  Slab mode (§8(e)): the z
+// planes [z0, z0 + nz) of the global grid; the buffers read with a halo carry zghost
+// planes below plane 0 and above plane nz - 1, filled by the neighbours.
 struct Grid {
-    int64_t nx, ny, nz;   // points per axis (unused = 1)
+    int64_t nx, ny, nz;   // points per axis (unused = 1); nz = owned planes
     int64_t sy, sz;       // strides: sy = nx, sz = nx*ny
-    int64_t n;            // total points
+    int64_t n;            // owned points
+    int zf_lo, zf_hi;     // 1 if local plane 0 / nz - 1 is a global z face (always 1 on one GPU)
+    int zghost;           // ghost planes on each side of the halo'd buffers (0 on one GPU)
 };
+
+// global z-face test for a local plane index (DIM == 3)
+__host__ __device__ __forceinline__ bool is_zface(const Grid &g, int64_t k) {
+    return (g.zf_lo && k == 0) || (g.zf_hi && k == g.nz - 1);
+}
 
 // Stage operands (RK4_GPU) P:495-519.  stage 1: Y = Psi, out = Psi_tmp;
 // stage 2: Y = Psi_tmp, out = Psi_out; stage 3: Y = Psi_out, out = Psi_tmp;
@@ -59,28 +69,43 @@ template <typename T> struct StageArgs {
     Consts<T> c;
     int *diverged;        // stage 4: atomicMin(step index) when a non-finite value is produced
     int step;             // absolute step index (for the divergence report)
+    // Slab mode: the stage output of the first / last `wsend` owned planes is also stored
+    // into the lower / upper neighbour's ghost planes (remote stores over NVLink, the halo
+    // exchange a9 fused into the producing kernel).  peer_lo[q] / peer_hi[q] address the
+    // neighbour's copy of local point q; nullptr on a global face or on one GPU.
+    cplx<T> *peer_lo, *peer_hi;
+    int wsend;
 };
+
+// Store one stage output value at local point q of plane k (and into the neighbours' ghosts).
+template <typename T>
+__device__ __forceinline__ void store_out(const StageArgs<T> &A, int64_t q, int64_t k, cplx<T> v) {
+    A.out[q] = v;
+    if (A.peer_lo && k < A.wsend) A.peer_lo[q] = v;
+    if (A.peer_hi && k >= A.g.nz - A.wsend) A.peer_hi[q] = v;
+}
 
 // RK4 stage combine at one point, (RK4_GPU) P:495-519 / (RK4) P:164-180:
 //   S1: K = F;      out = Psi + (k/2) F
 //   S2: K = K + 2F; out = Psi + (k/2) F
 //   S3: K = K + 2F; out = Psi + k F
 //   S4:             out = Psi + (k/6)(K + F)
+// kz = local plane of q (for the neighbour stores; 0 in 1D / 2D).
 template <int STAGE, typename T>
-__device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, cplx<T> F, cplx<T> psi) {
+__device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, int64_t kz, cplx<T> F, cplx<T> psi) {
     using C = cplx<T>;
     const T two = T(2);
     if (STAGE == 1) {
         A.K[q] = F;
-        A.out[q] = cadd(psi, cscale(A.c.kc, F));
+        store_out(A, q, kz, cadd(psi, cscale(A.c.kc, F)));
     } else if (STAGE == 2 || STAGE == 3) {
         C k = A.K[q];
         A.K[q] = cadd(k, cscale(two, F));
-        A.out[q] = cadd(psi, cscale(A.c.kc, F));
+        store_out(A, q, kz, cadd(psi, cscale(A.c.kc, F)));
     } else {
         C k = A.K[q];
         C r = cadd(psi, cscale(A.c.kc, cadd(k, F)));
-        A.out[q] = r;
+        store_out(A, q, kz, r);
         if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(A.diverged, A.step);
     }
 }

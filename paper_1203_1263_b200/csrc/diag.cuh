@@ -53,7 +53,8 @@ diag_partial(const cplx<T> *__restrict__ Psi, const T *__restrict__ V, Grid g, d
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;
         }
-        if (DIM >= 3 && (q / g.sz) + 1 < g.nz) {
+        // z pairs: inside the slab, or across to the upper neighbour's first plane (ghost)
+        if (DIM >= 3 && (q / g.sz) + 1 < g.nz + (g.zf_hi ? 0 : 1)) {
             const cplx<T> u = Psi[q + g.sz];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;

@@ -27,14 +27,14 @@ struct PointEval {
     __device__ __forceinline__ int n_bnd(int64_t i, int64_t j, int64_t k) const {
         int m = (i == 0 || i == g.nx - 1);
         if (DIM >= 2) m += (j == 0 || j == g.ny - 1);
-        if (DIM >= 3) m += (k == 0 || k == g.nz - 1);
+        if (DIM >= 3) m += is_zface(g, k);
         return m;
     }
     // Inward neighbour: one step in along every boundary axis (R-MSD-NBR).
     __device__ __forceinline__ void inward(int64_t &i, int64_t &j, int64_t &k) const {
         i = (i == 0) ? 1 : (i == g.nx - 1 ? g.nx - 2 : i);
         if (DIM >= 2) j = (j == 0) ? 1 : (j == g.ny - 1 ? g.ny - 2 : j);
-        if (DIM >= 3) k = (k == 0) ? 1 : (k == g.nz - 1 ? g.nz - 2 : k);
+        if (DIM >= 3) k = (g.zf_lo && k == 0) ? 1 : ((g.zf_hi && k == g.nz - 1) ? g.nz - 2 : k);
     }
     __device__ __forceinline__ int64_t idx(int64_t i, int64_t j, int64_t k) const {
         return k * g.sz + j * g.sy + i;
@@ -169,12 +169,13 @@ __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
     PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
     cplx<T> F = ev.F_any(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, F, psi);
+    rk_combine<STAGE, T>(A, q, k, F, psi);
 }
 
 // Boundary points only: a flat index over the boundary surface, mapped to (i,j,k).
-// 1D: 2 points; 2D: the 2(nx + ny) - 4 perimeter; 3D: two z faces, then for each
-// interior plane the perimeter of that plane.
+// 1D: 2 points; 2D: the 2(nx + ny) - 4 perimeter; 3D: the global z faces this grid
+// owns (plane 0 if zf_lo, plane nz-1 if zf_hi), then the perimeter of every other
+// owned plane.
 template <int DIM>
 __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t, int64_t &i, int64_t &j, int64_t &k) {
     if (DIM == 1) {
@@ -194,15 +195,16 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t, int64_t &i, 
         return true;
     }
     const int64_t face = g.nx * g.ny;
-    if (t < 2 * face) {
-        k = (t < face) ? 0 : g.nz - 1;
+    const int nf = g.zf_lo + g.zf_hi;
+    if (t < nf * face) {
+        k = (g.zf_lo && t < face) ? 0 : g.nz - 1;
         int64_t u = (t < face) ? t : t - face;
         i = u % g.nx; j = u / g.nx;
         return true;
     }
-    t -= 2 * face;
-    if (t >= per * (g.nz - 2)) return false;
-    k = 1 + t / per;
+    t -= nf * face;
+    if (t >= per * (g.nz - nf)) return false;
+    k = g.zf_lo + t / per;
     perim(t % per, i, j);
     return true;
 }
@@ -212,7 +214,8 @@ inline int64_t n_boundary_points(const Grid &g) {
     if (DIM == 1) return 2;
     const int64_t per = 2 * g.nx + 2 * (g.ny - 2);
     if (DIM == 2) return per;
-    return 2 * g.nx * g.ny + per * (g.nz - 2);
+    const int nf = g.zf_lo + g.zf_hi;
+    return nf * g.nx * g.ny + per * (g.nz - nf);
 }
 
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_bnd(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, F, psi);
+    rk_combine<STAGE, T>(A, q, k, F, psi);
 }
 
 }  // namespace nlse
@@ -234,17 +237,19 @@ namespace nlse {
 // Interior points only, one thread per point (flat index over the interior box).
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(256) stage_interior_generic(StageArgs<T> A) {
-    const int64_t mx = A.g.nx - 2, my = DIM >= 2 ? A.g.ny - 2 : 1, mz = DIM >= 3 ? A.g.nz - 2 : 1;
+    const int64_t k0 = DIM >= 3 ? A.g.zf_lo : 0;
+    const int64_t mx = A.g.nx - 2, my = DIM >= 2 ? A.g.ny - 2 : 1;
+    const int64_t mz = DIM >= 3 ? A.g.nz - A.g.zf_lo - A.g.zf_hi : 1;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= mx * my * mz) return;
     const int64_t i = 1 + t % mx;
     const int64_t j = DIM >= 2 ? 1 + (t / mx) % my : 0;
-    const int64_t k = DIM >= 3 ? 1 + t / (mx * my) : 0;
+    const int64_t k = DIM >= 3 ? k0 + t / (mx * my) : 0;
     PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_int(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, F, psi);
+    rk_combine<STAGE, T>(A, q, k, F, psi);
 }
 
 }  // namespace nlse

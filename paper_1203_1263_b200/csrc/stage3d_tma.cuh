@@ -1,0 +1,446 @@
+// stage3d_tma.cuh -- 3D interior stage kernel, v2: one fused HBM pass per RK4 stage
+// (§8(a) rows a1-a5, a7; a9's send side in slab mode), 2.5D z-streaming with TMA.
+//
+// CTA = 256 threads = 8 warps owns a TX x TY = 32 x 8 column of output points (lane =
+// x, warp = y) and streams it along a z chunk.  Per plane, one elected thread issues
+// TMA (cp.async.bulk.tensor) loads into mbarrier-tracked shared-memory rings, P planes
+// ahead of use:
+//   * the stage input Y as a (TX+2H) x (TY+2H) tile (H = w: 1 CD, 2 2SHOC) -- ring of
+//     NS = P+4 planes (the planes in use, P in flight, one that laggard warps may still
+//     read, one free);
+//   * Psi, K_tot (stages 2-4) and V at the owned points -- ring of NP = P+2 planes.
+// There is no per-element address arithmetic: out-of-grid parts of a box are zero-
+// filled by TMA and never used.  Compute per plane z (2SHOC):
+//   1. D(z+1) = Delta_2 Y / h^2 (2SHOC step 1) at the owned point and, by
+//      warps 0-2, on the one-point ring around the tile, into a shared D plane (3-plane
+//      ring, so one __syncthreads per plane suffices).  D never touches HBM.  Face
+//      points take the Laplacian form of the BC.
+//   2. 2SHOC step 2 from D(z) in shared memory and the register queue
+//      D(z-1), D(z), D(z+1), pair sums Px, Py of planes z-1, z, z+1 (the edge cross
+//      term is sums of pair sums); F (fsplit) P:424-428; the RK4 stage
+//      combine (RK4_GPU) P:495-519; K_tot and the stage output stored once (STG.128,
+//      one warp = 512 contiguous bytes).
+// Tiles whose ring touches an x/y face or lies partly outside the grid run the same
+// loop with per-point face handling (EDGE = true); all others run branch-free.
+// Domain-boundary outputs are written by stage_boundary (generic.cuh).  Every value
+// follows the DAG of DESIGN.md §3.1, so the output is bit-identical to the oracle.
+#pragma once
+#include <cuda.h>
+#include "generic.cuh"
+
+namespace nlse {
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+
+// ------------------------------------------------------------------ configuration
+template <typename T, int ORDER, int P>
+struct T3Cfg {
+    static constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
+    static constexpr int TX = 32, TY = 8, NT = TX * TY;
+    static constexpr int PX = TX + 2 * H, PY = TY + 2 * H;
+    static constexpr int CB = 2 * int(sizeof(T));                   // bytes per complex value
+    static constexpr int NS = P + 4, NP = P + 2, ND = (ORDER == ORDER_2SHOC) ? 3 : 0;
+    static constexpr int DPX = TX + 2, DPY = TY + 2;
+    static constexpr int up128(int b) { return (b + 127) / 128 * 128; }
+    static constexpr int YBYTES = PX * PY * CB;
+    static constexpr int YSLOT = up128(YBYTES);
+    static constexpr int OWN_C = NT * CB, OWN_R = NT * int(sizeof(T));
+    static constexpr int PKVSLOT = up128(2 * OWN_C + OWN_R);          // Psi | K_tot | V
+    static constexpr int DSLOT = up128(DPX * DPY * CB);
+    static constexpr int OFF_PKV = NS * YSLOT;
+    static constexpr int OFF_D = OFF_PKV + NP * PKVSLOT;
+    static constexpr int OFF_BAR = OFF_D + ND * DSLOT;
+    static constexpr int SMEM = OFF_BAR + (NS + NP) * 8;
+    // box dimensions (in T elements along x) of the four tensor maps
+    static constexpr int BOX_Y_X = 2 * PX, BOX_Y_Y = PY;
+    static constexpr int BOX_C_X = 2 * TX, BOX_R_X = TX, BOX_O_Y = TY;
+};
+
+// The TMA descriptors of one context: Y maps of the three halo'd buffers (Psi, Psi_tmp,
+// Psi_out; halo box), and Psi, K_tot, V over the owned box.  z coordinate of local
+// plane p is p + zghost for the halo'd buffers, p for K_tot and V.
+struct Tma3Maps {
+    CUtensorMap y[3];
+    CUtensorMap psi, k, v;
+};
+
+template <typename T, int ORDER, int BC, int STAGE, int P, bool EDGE>
+struct T3Body {
+    using C = cplx<T>;
+    using Cfg = T3Cfg<T, ORDER, P>;
+    static constexpr int H = Cfg::H, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP;
+    static constexpr int DPX = Cfg::DPX;
+
+    const StageArgs<T> &A;
+    unsigned char *sm;
+    int x0, y0;
+
+    __device__ __forceinline__ C *yslot(int s) const { return reinterpret_cast<C *>(sm + s * Cfg::YSLOT) + H * PX + H; }
+    __device__ __forceinline__ C *dslot(int s) const {
+        return reinterpret_cast<C *>(sm + Cfg::OFF_D + s * Cfg::DSLOT) + DPX + 1;
+    }
+    __device__ __forceinline__ unsigned char *pkvslot(int s) const { return sm + Cfg::OFF_PKV + s * Cfg::PKVSLOT; }
+
+    __device__ __forceinline__ T nlin(int64_t q, C yq) const {
+        T rho = (yq.x * yq.x) + (yq.y * yq.y);
+        T n = A.c.s * rho;
+        if (A.V) n = n - __ldg(A.V + q);
+        return n;
+    }
+    __device__ __forceinline__ int64_t gq(int p, int lx, int ly) const {
+        return int64_t(p) * A.g.sz + int64_t(y0 + ly) * A.g.sy + (x0 + lx);
+    }
+    // Boundary D at a face point b (Laplacian form of the BC, (BCDlap) P:320-323 /
+    // (BCMSDlap) P:336-344), given Y_b, and Y, D at the inward normal neighbour b'.
+    __device__ __forceinline__ C D_bc(int64_t qb, C yb, int64_t qb1, C y1, C d1) const {
+        const T nb = nlin(qb, yb);
+        if (BC == BC_DIRICHLET) {
+            const T t = A.c.inv_a * nb;
+            C r; r.x = -(t * yb.x); r.y = -(t * yb.y);
+            return r;
+        } else {
+            const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+            T re = T(0);
+            if (!(rho1 < A.c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+            const T n1 = nlin(qb1, y1);
+            const T gg = re + ((n1 - nb) * A.c.inv_a);
+            return cscale(gg, yb);
+        }
+    }
+    // 2SHOC step 1 / CD at an in-plane-interior point: (((Px-Y2)+(Py-Y2))+(Pz-Y2))*ih2
+    __device__ __forceinline__ C D_int(const C *ym, const C *y0p, const C *yp) const {
+        const C yc = y0p[0];
+        const C y2 = cadd(yc, yc);
+        C acc = csub(cadd(y0p[-1], y0p[1]), y2);
+        acc = cadd(acc, csub(cadd(y0p[-PX], y0p[PX]), y2));
+        acc = cadd(acc, csub(cadd(ym[0], yp[0]), y2));
+        return cscale(A.c.ih2, acc);
+    }
+    // D(p) at local (lx, ly) of plane p with full face handling (edge tiles and z-face
+    // planes).  sm_, s0, sp: Y slots of planes p-1, p, p+1 (sp unused when p is a z face);
+    // dprev: D slot of plane p-1 (the inward neighbour of a z-face plane p = nz-1).
+    __device__ C D_gen(int p, int smm, int s0, int sp, int dprev, int lx, int ly) const {
+        const int gx = x0 + lx, gy = y0 + ly;
+        const int nx = int(A.g.nx), ny = int(A.g.ny);
+        C nanv; nanv.x = T(NAN); nanv.y = T(NAN);
+        if (gx < 0 || gx >= nx || gy < 0 || gy >= ny) return nanv;
+        const bool fx = (gx == 0 || gx == nx - 1), fy = (gy == 0 || gy == ny - 1);
+        const bool fz = A.g.zf_hi && (p == int(A.g.nz) - 1);   // plane p is never the lower z face
+        if (int(fx) + int(fy) + int(fz) >= 2) return nanv;      // edge / corner: never used (R-DFACE)
+        const int o = ly * PX + lx;
+        if (fz) {
+            const int od = ly * DPX + lx;
+            return D_bc(gq(p, lx, ly), yslot(s0)[o], gq(p - 1, lx, ly), yslot(smm)[o], dslot(dprev)[od]);
+        }
+        if (!fx && !fy) return D_int(yslot(smm) + o, yslot(s0) + o, yslot(sp) + o);
+        int lx1 = lx, ly1 = ly;
+        if (gx == 0) lx1 = lx + 1; else if (gx == nx - 1) lx1 = lx - 1;
+        else if (gy == 0) ly1 = ly + 1; else ly1 = ly - 1;
+        const int o1 = ly1 * PX + lx1;
+        const C d1 = D_int(yslot(smm) + o1, yslot(s0) + o1, yslot(sp) + o1);
+        return D_bc(gq(p, lx, ly), yslot(s0)[o], gq(p, lx1, ly1), yslot(s0)[o1], d1);
+    }
+};
+
+// F (fsplit) P:424-428 and the RK4 stage combine (RK4_GPU) P:495-519 at one point.
+template <typename T, int STAGE>
+__device__ __forceinline__ void t3_finish(const StageArgs<T> &A, int64_t q, int z, cplx<T> yc, cplx<T> L,
+                                          cplx<T> psi, cplx<T> kt, T v) {
+    using C = cplx<T>;
+    const T rho = (yc.x * yc.x) + (yc.y * yc.y);
+    const T sr = A.c.s * rho;
+    T fr = (-(A.c.a * L.y)) - (sr * yc.y);
+    T fi = (A.c.a * L.x) + (sr * yc.x);
+    if (A.V) { fr = fr + (v * yc.y); fi = fi - (v * yc.x); }
+    C F; F.x = fr; F.y = fi;
+    if (STAGE == 1) {
+        A.K[q] = F;
+        store_out(A, q, z, cadd(yc, cscale(A.c.kc, F)));
+    } else if (STAGE == 4) {
+        const C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
+        store_out(A, q, z, r4);
+        if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, A.step);
+    } else {
+        A.K[q] = cadd(kt, cscale(T(2), F));
+        store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
+    }
+}
+
+template <typename T, int ORDER, int BC, int STAGE, int P, bool EDGE>
+__device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap *mP, const CUtensorMap *mK,
+                                       const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
+                                       int y0, int zs, int ze) {
+    using C = cplx<T>;
+    using Cfg = T3Cfg<T, ORDER, P>;
+    using B = T3Body<T, ORDER, BC, STAGE, P, EDGE>;
+    constexpr int H = Cfg::H, TX = Cfg::TX, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
+    const B b{A, sm, x0, y0};
+    const Grid &g = A.g;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int nz = int(g.nz);
+    const int zmem_lo = g.zf_lo ? 0 : -g.zghost, zmem_hi = nz + (g.zf_hi ? 0 : g.zghost);
+    const int zl_lo = max(zs - H, zmem_lo), zl_hi = min(ze + H - 1, zmem_hi - 1);  // Y planes loaded
+    const int zbase = zs - H;
+    const unsigned bar0 = smem_u32(sm + Cfg::OFF_BAR);   // NS Y barriers, then NP PKV barriers
+    const unsigned pkv_bytes = (STAGE != 1 ? 2u * Cfg::OWN_C : 0u) + (A.V ? unsigned(Cfg::OWN_R) : 0u);
+
+    auto issue_y = [&](int p) {
+        if (p > zl_hi) return;                        // past the last plane: never waited on
+        const int s = (p - zbase) % NS;
+        const unsigned bar = bar0 + 8 * s;
+        if (p < zl_lo) {                              // not in memory (below a z face): complete
+            mbar_arrive(bar);                         // the phase anyway so parities stay in step
+            return;
+        }
+        mbar_expect_tx(bar, Cfg::YBYTES);
+        tma_load_3d(smem_u32(sm + s * Cfg::YSLOT), mY, 2 * (x0 - H), y0 - H, p + g.zghost, bar);
+    };
+    auto issue_pkv = [&](int p) {
+        if (p >= ze || pkv_bytes == 0) return;
+        const int s = (p - zs) % NP;
+        const unsigned bar = bar0 + 8 * (NS + s);
+        unsigned char *dst = sm + Cfg::OFF_PKV + s * Cfg::PKVSLOT;
+        mbar_expect_tx(bar, pkv_bytes);
+        if (STAGE != 1) {
+            tma_load_3d(smem_u32(dst), mP, 2 * x0, y0, p + g.zghost, bar);
+            tma_load_3d(smem_u32(dst + Cfg::OWN_C), mK, 2 * x0, y0, p, bar);
+        }
+        if (A.V) tma_load_3d(smem_u32(dst + 2 * Cfg::OWN_C), mV, x0, y0, p, bar);
+    };
+
+    if (tid == 0) {
+        for (int i = 0; i < NS + NP; i++) mbar_init(bar0 + 8 * i, 1);
+        fence_proxy_async();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int p = zbase; p <= zs + H + P - 1; p++) issue_y(p);
+        for (int p = zs; p <= zs + P - 1; p++) issue_pkv(p);
+    }
+
+    const int gx = x0 + tx, gy = y0 + ty;
+    const int nx = int(g.nx), ny = int(g.ny);
+    const bool out_ok = !EDGE || (gx >= 1 && gx <= nx - 2 && gy >= 1 && gy <= ny - 2);
+    const int own = ty * PX + tx;                      // offset of the owned point in a Y tile
+    const int downo = ty * DPX + tx;                   // ... in a D tile
+    const int pown = ty * TX + tx;                     // ... in an owned-box (Psi/K/V) tile
+    const int64_t qrow = int64_t(gy) * g.sy + gx;     // global offset in plane 0
+    // ring assignment (2SHOC): warp 0 row -1, warp 1 row TY, warp 2 columns -1 and TX
+    int rlx = 0, rly = 0;
+    bool ring = false;
+    if (ORDER == ORDER_2SHOC) {
+        if (ty == 0) { ring = true; rlx = tx; rly = -1; }
+        else if (ty == 1) { ring = true; rlx = tx; rly = Cfg::TY; }
+        else if (ty == 2 && tx < 2 * Cfg::TY) { ring = true; rlx = tx < Cfg::TY ? -1 : TX; rly = tx % Cfg::TY; }
+    }
+    const int ro = rly * PX + rlx, rdo = rly * DPX + rlx;
+
+    // PKV ring position of plane z
+    int ps = 0; unsigned pp = 0;
+    auto pkv_wait = [&]() { if (pkv_bytes) mbar_wait(bar0 + 8 * (NS + ps), pp); };
+    auto pkv_next = [&]() { if (++ps == NP) { ps = 0; pp ^= 1u; } };
+    auto load_own = [&](C &psi, C &kt, T &v) {
+        const unsigned char *src = b.pkvslot(ps);
+        if (STAGE != 1) {
+            psi = reinterpret_cast<const C *>(src)[pown];
+            kt = reinterpret_cast<const C *>(src + Cfg::OWN_C)[pown];
+        }
+        if (A.V) v = reinterpret_cast<const T *>(src + 2 * Cfg::OWN_C)[pown];
+    };
+
+    if (ORDER == ORDER_CD) {
+        // ------------------------------------------------------------ CD: L = D
+        // slots of planes z-1, z, z+1 (relative index p - zbase: 0, 1, 2 at z = zs)
+        int sm1 = 0, s0 = 1, s1 = 2;
+        unsigned par1 = 0;                            // parity of plane z+1's slot use
+        if (zs - 1 >= zl_lo) mbar_wait(bar0 + 8 * sm1, 0);
+        mbar_wait(bar0 + 8 * s0, 0);
+        C ym = b.yslot(sm1)[own], yc = b.yslot(s0)[own];
+        for (int z = zs; z < ze; z++) {
+            if (tid == 0) { issue_y(z + H + P); issue_pkv(z + P); }
+            mbar_wait(bar0 + 8 * s1, par1);
+            const C *Y0 = b.yslot(s0) + own;
+            const C yp = b.yslot(s1)[own];
+            C psi, kt; T v;
+            pkv_wait();
+            load_own(psi, kt, v);
+            if (out_ok) {
+                const C y2 = cadd(yc, yc);
+                C acc = csub(cadd(Y0[-1], Y0[1]), y2);
+                acc = cadd(acc, csub(cadd(Y0[-PX], Y0[PX]), y2));
+                acc = cadd(acc, csub(cadd(ym, yp), y2));
+                const C L = cscale(A.c.ih2, acc);
+                t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yc, L, psi, kt, v);
+            }
+            ym = yc; yc = yp;
+            sm1 = s0; s0 = s1;
+            if (++s1 == NS) { s1 = 0; par1 ^= 1u; }
+            pkv_next();
+            __syncthreads();
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- 2SHOC
+    // Y slots of planes z-1, z, z+1, z+2 at z = zs: relative indices 1, 2, 3, 4
+    int sm1 = 1, s0 = 2, s1 = 3, s2 = 4;
+    unsigned par2 = 0;                                // parity of plane z+2's slot use
+    if (zs - 2 >= zl_lo) mbar_wait(bar0 + 0, 0);
+    mbar_wait(bar0 + 8 * sm1, 0);
+    mbar_wait(bar0 + 8 * s0, 0);
+    mbar_wait(bar0 + 8 * s1, 0);
+    int d0s = 0;                                      // D slot of plane z (3-plane ring)
+    C yz = b.yslot(s0)[own], yz1 = b.yslot(s1)[own];
+    C px0, py0, pxm, pym, d0, dm;
+    {
+        const C *Y0 = b.yslot(s0) + own, *Ym = b.yslot(sm1) + own;
+        px0 = cadd(Y0[-1], Y0[1]);
+        py0 = cadd(Y0[-PX], Y0[PX]);
+        pxm = cadd(Ym[-1], Ym[1]);
+        pym = cadd(Ym[-PX], Ym[PX]);
+        // D(zs) at the owned point and the ring (zs is never a z face)
+        if (EDGE) d0 = b.D_gen(zs, sm1, s0, s1, 0, tx, ty);
+        else d0 = b.D_int(Ym, Y0, b.yslot(s1) + own);
+        b.dslot(d0s)[downo] = d0;
+        if (ring) {
+            C dr;
+            if (EDGE) dr = b.D_gen(zs, sm1, s0, s1, 0, rlx, rly);
+            else dr = b.D_int(b.yslot(sm1) + ro, b.yslot(s0) + ro, b.yslot(s1) + ro);
+            b.dslot(d0s)[rdo] = dr;
+        }
+        // D(zs - 1) at the owned point (used only there): BC form on the lower z face,
+        // else the stencil
+        dm = d0;
+        if (!out_ok) {
+        } else if (g.zf_lo && zs - 1 == 0) {
+            dm = b.D_bc(int64_t(qrow), Ym[0], int64_t(g.sz) + qrow, yz, d0);
+        } else {
+            const C *Ymm = b.yslot(0) + own;
+            const C y2 = cadd(Ym[0], Ym[0]);
+            C acc = csub(pxm, y2);
+            acc = cadd(acc, csub(pym, y2));
+            acc = cadd(acc, csub(cadd(Ymm[0], yz), y2));
+            dm = cscale(A.c.ih2, acc);
+        }
+    }
+    __syncthreads();
+
+    for (int z = zs; z < ze; z++) {
+        if (tid == 0) { issue_y(z + H + P); issue_pkv(z + P); }
+        const bool zf1 = g.zf_hi && (z + 1 == nz - 1);       // D(z+1) by the BC form
+        const int d1s = (d0s == 2) ? 0 : d0s + 1;
+        if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
+        const C *Y0 = b.yslot(s0) + own, *Y1 = b.yslot(s1) + own;
+        const C px1 = cadd(Y1[-1], Y1[1]);
+        const C py1 = cadd(Y1[-PX], Y1[PX]);
+        C yz2 = yz1, dn;
+        if (EDGE) {
+            dn = b.D_gen(z + 1, s0, s1, s2, d0s, tx, ty);
+            if (!zf1) yz2 = b.yslot(s2)[own];
+        } else if (zf1) {
+            dn = b.D_bc(int64_t(z + 1) * g.sz + qrow, yz1, int64_t(z) * g.sz + qrow, yz, d0);
+        } else {
+            yz2 = b.yslot(s2)[own];
+            const C y2 = cadd(yz1, yz1);
+            C acc = csub(px1, y2);
+            acc = cadd(acc, csub(py1, y2));
+            acc = cadd(acc, csub(cadd(yz, yz2), y2));
+            dn = cscale(A.c.ih2, acc);
+        }
+        b.dslot(d1s)[downo] = dn;
+        if (ring) {
+            C dr;
+            if (EDGE) {
+                dr = b.D_gen(z + 1, s0, s1, s2, d0s, rlx, rly);
+            } else if (zf1) {
+                dr = b.D_bc(b.gq(z + 1, rlx, rly), b.yslot(s1)[ro], b.gq(z, rlx, rly), b.yslot(s0)[ro],
+                            b.dslot(d0s)[rdo]);
+            } else {
+                dr = b.D_int(b.yslot(s0) + ro, b.yslot(s1) + ro, b.yslot(s2) + ro);
+            }
+            b.dslot(d1s)[rdo] = dr;
+        }
+        __syncthreads();
+
+        C psi, kt; T v;
+        pkv_wait();
+        load_own(psi, kt, v);
+        if (out_ok) {
+            // 2SHOC step 2, grouping of DESIGN.md §3.1
+            const C y4 = cscale(T(4), yz);
+            const C pxa = cadd(Y0[-PX - 1], Y0[-PX + 1]);
+            const C pxb = cadd(Y0[PX - 1], Y0[PX + 1]);
+            const C exy = csub(cadd(pxa, pxb), y4);
+            const C exz = csub(cadd(pxm, px1), y4);
+            const C eyz = csub(cadd(pym, py1), y4);
+            const C E = cadd(cadd(exy, exz), eyz);
+            const C *Dz = b.dslot(d0s) + downo;
+            const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dm, dn));
+            const C td = csub(sd, cscale(T(10), d0));
+            const C L = csub(cscale(A.c.c16h2, E), cscale(A.c.c112, td));
+            t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yz, L, psi, kt, v);
+        }
+        // rotate the register queues and the rings
+        dm = d0; d0 = dn;
+        pxm = px0; px0 = px1;
+        pym = py0; py0 = py1;
+        yz = yz1; yz1 = yz2;
+        sm1 = s0; s0 = s1; s1 = s2;
+        if (++s2 == NS) { s2 = 0; par2 ^= 1u; }
+        d0s = d1s;
+        pkv_next();
+    }
+}
+
+template <typename T, int ORDER, int BC, int STAGE, int P>
+__global__ void __launch_bounds__(256, (sizeof(T) == 8 ? 2 : 3))
+stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
+            const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV, StageArgs<T> A,
+            int zchunk) {
+    using Cfg = T3Cfg<T, ORDER, P>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
+    const int nz = int(A.g.nz);
+    const int zlo = A.g.zf_lo ? 1 : 0, zhi = nz - (A.g.zf_hi ? 1 : 0);
+    const int zs = zlo + blockIdx.z * zchunk;
+    const int ze = min(zs + zchunk, zhi);
+    if (zs >= ze) return;
+    const int nx = int(A.g.nx), ny = int(A.g.ny);
+    // every owned and ring point in-plane interior -> branch-free path
+    const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
+    if (edge) t3_run<T, ORDER, BC, STAGE, P, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    else t3_run<T, ORDER, BC, STAGE, P, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+}
+
+}  // namespace nlse

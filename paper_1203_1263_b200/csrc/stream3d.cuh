@@ -161,7 +161,7 @@ struct S3 {
 
 // F (fsplit) P:424-428 and the RK4 stage combine (RK4_GPU) P:495-519 at one point.
 template <typename T, int STAGE>
-__device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, cplx<T> yc, cplx<T> L,
+__device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, int z, cplx<T> yc, cplx<T> L,
                                              cplx<T> psi, cplx<T> kt, T v) {
     using C = cplx<T>;
     T rho = (yc.x * yc.x) + (yc.y * yc.y);
@@ -172,14 +172,14 @@ __device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, c
     C F; F.x = fr; F.y = fi;
     if (STAGE == 1) {
         A.K[q] = F;
-        A.out[q] = cadd(yc, cscale(A.c.kc, F));
+        store_out(A, q, z, cadd(yc, cscale(A.c.kc, F)));
     } else if (STAGE == 4) {
         C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
-        A.out[q] = r4;
+        store_out(A, q, z, r4);
         if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, A.step);
     } else {
         A.K[q] = cadd(kt, cscale(T(2), F));
-        A.out[q] = cadd(psi, cscale(A.c.kc, F));
+        store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
     }
 }
 
@@ -195,8 +195,12 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
     const int tx = threadIdx.x % S3_TX, ty = threadIdx.x / S3_TX;
     const int x0 = 1 + blockIdx.x * Cfg::TX;
     const int y0 = 1 + blockIdx.y * Cfg::TY;
-    const int zs = 1 + blockIdx.z * zchunk;
-    const int ze = min(zs + zchunk, int(A.g.nz - 1));   // outputs [zs, ze)
+    // output planes: the owned planes that are not global z faces, split in z chunks
+    const int zlo = A.g.zf_lo ? 1 : 0, zhi = int(A.g.nz) - (A.g.zf_hi ? 1 : 0);
+    const int zmem_lo = A.g.zf_lo ? 0 : -A.g.zghost;               // planes present in memory
+    const int zmem_hi = int(A.g.nz) + (A.g.zf_hi ? 0 : A.g.zghost);
+    const int zs = zlo + blockIdx.z * zchunk;
+    const int ze = min(zs + zchunk, zhi);   // outputs [zs, ze)
     if (zs >= ze) return;
     const K k(A, reinterpret_cast<C *>(smem_raw), x0, y0);
     const Grid &g = A.g;
@@ -214,7 +218,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
 
     if (ORDER == ORDER_CD) {
         // ------------------------------------------------------------------ CD: L = D
-        int sm = (zs - 1) % NB, s0 = zs % NB, sp = (zs + 1) % NB;
+        int sm = (zs - 1 + NB) % NB, s0 = zs % NB, sp = (zs + 1) % NB;
         k.load_plane(zs - 1, sm);
         k.load_plane(zs, s0);
         k.load_plane(zs + 1, sp);
@@ -253,7 +257,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
                 acc = cadd(acc, csub(cadd(ya, yb), y2));
                 acc = cadd(acc, csub(cadd(ym[r], yp[r]), y2));
                 const C L = cscale(A.c.ih2, acc);
-                finish_point<T, STAGE>(A, zo + qrow[r], yc[r], L, psi[r], kt[r], v[r]);
+                finish_point<T, STAGE>(A, zo + qrow[r], z, yc[r], L, psi[r], kt[r], v[r]);
             }
 #pragma unroll
             for (int r = 0; r < RY; r++) { ym[r] = yc[r]; yc[r] = yp[r]; }
@@ -266,13 +270,13 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
 
     // ---------------------------------------------------------------------- 2SHOC
     // slots of planes z-1, z, z+1, z+2 (and z-2 in the prologue)
-    int s_m1 = (zs - 1) % NB, s_0 = zs % NB, s_1 = (zs + 1) % NB, s_2 = (zs + 2) % NB;
+    int s_m1 = (zs - 1 + NB) % NB, s_0 = zs % NB, s_1 = (zs + 1) % NB, s_2 = (zs + 2) % NB;
     const int s_m2 = (zs + NB - 2) % NB;
-    if (zs - 2 >= 0) k.load_plane(zs - 2, s_m2);
+    if (zs - 2 >= zmem_lo) k.load_plane(zs - 2, s_m2);
     k.load_plane(zs - 1, s_m1);
     k.load_plane(zs, s_0);
     k.load_plane(zs + 1, s_1);
-    if (zs + 2 <= g.nz - 1) k.load_plane(zs + 2, s_2);
+    if (zs + 2 < zmem_hi) k.load_plane(zs + 2, s_2);
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
@@ -303,7 +307,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
     for (int r = 0; r < RY; r++) {
         const int ly = ly0 + r;
         if (!out_ok[r]) { dm[r] = cnan<T>(); continue; }
-        if (zs - 1 == 0) {
+        if (g.zf_lo && zs - 1 == 0) {
             // z face: BC form with b' = (x, y, 1), whose D was computed above
             dm[r] = k.D_face_val(qrow[r], k.Ys(s_m1, tx, ly), qrow[r] + g.sz, yq0[r], d0[r]);
         } else {
@@ -315,7 +319,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
     for (int z = zs; z < ze; z++) {
         // (1) Y plane z+3 (into the slot of plane z-2) and this plane's Psi, K, V
         const int s_3 = (s_2 + 1 == NB) ? 0 : s_2 + 1;
-        if (z + 1 < ze && z + 3 <= g.nz - 1) k.load_plane(z + 3, s_3);
+        if (z + 1 < ze && z + 3 < zmem_hi) k.load_plane(z + 3, s_3);
         cp_async_commit();
         const int64_t zo = int64_t(z) * g.sz;
         C psi[RY], kt[RY];
@@ -331,7 +335,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
 
         // (2) D(z+1) at the owned columns, pair sums at z+1
         const int zp = z + 1;
-        const bool zface = (zp == g.nz - 1);
+        const bool zface = g.zf_hi && (zp == g.nz - 1);
         const int dsn = dsl ^ 1;
         C dn[RY], px1[RY], py1[RY], yq2[RY];
 #pragma unroll
@@ -393,7 +397,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
                               cadd(dm[r], dn[r]));
             const C td = csub(sd, cscale(T(10), d0[r]));
             const C L = csub(cscale(A.c.c16h2, E), cscale(A.c.c112, td));
-            finish_point<T, STAGE>(A, zo + qrow[r], yc, L, psi[r], kt[r], v[r]);
+            finish_point<T, STAGE>(A, zo + qrow[r], z, yc, L, psi[r], kt[r], v[r]);
         }
         // (4) rotate the register queues and the slots
 #pragma unroll
@@ -413,7 +417,7 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
 template <typename T, int ORDER, int BC, int STAGE, int RY>
 void launch_stream3d_ry(const StageArgs<T> &A, cudaStream_t st) {
     using Cfg = S3Cfg<T, ORDER, RY>;
-    const int64_t mx = A.g.nx - 2, my = A.g.ny - 2, mz = A.g.nz - 2;
+    const int64_t mx = A.g.nx - 2, my = A.g.ny - 2, mz = A.g.nz - A.g.zf_lo - A.g.zf_hi;
     const unsigned gx = unsigned((mx + Cfg::TX - 1) / Cfg::TX);
     const unsigned gy = unsigned((my + Cfg::TY - 1) / Cfg::TY);
     // z chunks: enough CTAs for ~4 waves of resident CTAs, chunks >= 32 planes

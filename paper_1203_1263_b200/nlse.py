@@ -45,7 +45,13 @@ class nlse_timing(ctypes.Structure):
 class nlse_info(ctypes.Structure):
     _fields_ = [("points", ctypes.c_int64), ("launches_per_step", ctypes.c_int64),
                 ("min_bytes_per_step", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("elem_bytes", ctypes.c_int), ("variant", ctypes.c_char * 64)]
+                ("elem_bytes", ctypes.c_int), ("variant", ctypes.c_char * 64),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("z0", ctypes.c_int64),
+                ("nz_local", ctypes.c_int64)]
+
+
+NLSE_MAX_RANKS = 16
+NLSE_DIST_HANDLE_BYTES = 512
 
 
 def _load():
@@ -75,9 +81,21 @@ def _load():
     lib.nlse_get_timing.argtypes = [P, ctypes.POINTER(nlse_timing)]
     lib.nlse_reset_timing.argtypes = [P]
     lib.nlse_get_info.argtypes = [P, ctypes.POINTER(nlse_info)]
+    I64P = ctypes.POINTER(ctypes.c_int64)
+    lib.nlse_slab_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, I64P, I64P]
+    lib.nlse_create_dist.argtypes = [ctypes.c_int, I64P, ctypes.c_double, ctypes.c_double, ctypes.c_double, D,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_int,
+                                     ctypes.c_int, ctypes.POINTER(P)]
+    lib.nlse_dist_export.argtypes = [P, ctypes.c_char_p]
+    lib.nlse_dist_connect.argtypes = [P, ctypes.c_char_p]
+    lib.nlse_dist_connect_local.argtypes = [ctypes.POINTER(P), ctypes.c_int]
+    lib.nlse_step_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_double, ctypes.c_int64]
+    lib.nlse_diagnostics_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, D, D]
     for f in ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device", "nlse_get_psi_device",
               "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_get_stream", "nlse_set_timing",
-              "nlse_get_timing", "nlse_reset_timing", "nlse_get_info"):
+              "nlse_get_timing", "nlse_reset_timing", "nlse_get_info", "nlse_slab_range", "nlse_create_dist",
+              "nlse_dist_export", "nlse_dist_connect", "nlse_dist_connect_local", "nlse_step_group",
+              "nlse_diagnostics_group"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -88,7 +106,8 @@ lib = _load()
 EXPORTS = ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device", "nlse_get_psi_device",
            "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_last_error", "nlse_status_string",
            "nlse_destroy", "nlse_get_stream", "nlse_set_timing", "nlse_get_timing", "nlse_reset_timing",
-           "nlse_get_info")
+           "nlse_get_info", "nlse_slab_range", "nlse_create_dist", "nlse_dist_export", "nlse_dist_connect",
+           "nlse_dist_connect_local", "nlse_step_group", "nlse_diagnostics_group")
 
 
 def _check(st, ctx=None):
@@ -104,14 +123,28 @@ def nlse_stability_bound(ndim: int, a: float, h: float, scheme: str = "2shoc"):
     return km.value, kr.value
 
 
+def nlse_slab_range(nz: int, nranks: int, rank: int):
+    """(z0, nloc): the global planes [z0, z0 + nloc) rank `rank` owns in slab mode."""
+    z0, nl = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.nlse_slab_range(int(nz), int(nranks), int(rank), ctypes.byref(z0), ctypes.byref(nl)))
+    return z0.value, nl.value
+
+
 class Solver:
-    """Owns one nlse_ctx.  dims = (nx,), (nx, ny) or (nx, ny, nz); numpy arrays have shape
-    reversed(dims) (x fastest)."""
+    """Owns one nlse_ctx.  dims = (nx,), (nx, ny) or (nx, ny, nz) (the GLOBAL grid); numpy arrays
+    have shape reversed(dims) (x fastest).  dist=(rank, nranks) creates a slab-mode context
+    (nlse_create_dist): Psi / V arrays then hold the local slab, shape (nloc, ny, nx)."""
 
     def __init__(self, dims, h, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc", precision="fp64",
-                 force_dt=False, generic=False):
+                 force_dt=False, generic=False, dist=None):
         self.dims = tuple(int(d) for d in dims)
-        self.shape = tuple(reversed(self.dims))
+        self.dist = dist
+        if dist is not None:
+            rank, nranks = dist
+            self.z0, nloc = nlse_slab_range(self.dims[2], nranks, rank)
+            self.shape = (nloc,) + tuple(reversed(self.dims[:2]))
+        else:
+            self.shape = tuple(reversed(self.dims))
         self.precision = precision
         d3 = (ctypes.c_int64 * 3)(*(list(self.dims) + [1] * (3 - len(self.dims))))
         Vp = None
@@ -121,8 +154,12 @@ class Solver:
             Vp = self._V.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         flags = (NLSE_FLAG_FORCE_DT if force_dt else 0) | (NLSE_FLAG_GENERIC_KERNELS if generic else 0)
         ctx = ctypes.c_void_p()
-        st = lib.nlse_create(len(self.dims), d3, h, a, s, Vp, BC[bc], ORDER[scheme], PREC[precision], flags,
-                             ctypes.byref(ctx))
+        if dist is None:
+            st = lib.nlse_create(len(self.dims), d3, h, a, s, Vp, BC[bc], ORDER[scheme], PREC[precision], flags,
+                                 ctypes.byref(ctx))
+        else:
+            st = lib.nlse_create_dist(len(self.dims), d3, h, a, s, Vp, BC[bc], ORDER[scheme], PREC[precision],
+                                      flags, int(dist[0]), int(dist[1]), ctypes.byref(ctx))
         self._V = None
         _check(st, None)
         self.ctx = ctx
@@ -190,10 +227,49 @@ class Solver:
         _check(lib.nlse_get_info(self.ctx, ctypes.byref(t)), self.ctx)
         return dict(points=t.points, launches_per_step=t.launches_per_step,
                     min_bytes_per_step=t.min_bytes_per_step, device_bytes=t.device_bytes,
-                    elem_bytes=t.elem_bytes, variant=t.variant.decode())
+                    elem_bytes=t.elem_bytes, variant=t.variant.decode(), rank=t.rank, nranks=t.nranks,
+                    z0=t.z0, nz_local=t.nz_local)
+
+    def nlse_dist_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(NLSE_DIST_HANDLE_BYTES)
+        _check(lib.nlse_dist_export(self.ctx, buf), self.ctx)
+        return buf.raw
+
+    def nlse_dist_connect(self, handles):
+        """handles: the nranks exported handles in rank order (list of bytes or one bytes object)."""
+        blob = b"".join(handles) if not isinstance(handles, (bytes, bytearray)) else bytes(handles)
+        _check(lib.nlse_dist_connect(self.ctx, blob), self.ctx)
 
     # --- conveniences ----------------------------------------------------------------------------
     set_psi = nlse_set_psi
     get_psi = nlse_get_psi
     step = nlse_step
     diagnostics = nlse_diagnostics
+
+
+# --- virtual ranks / groups of contexts in one process ----------------------------------------------
+
+def _ctx_array(solvers):
+    arr = (ctypes.c_void_p * len(solvers))(*[sv.ctx for sv in solvers])
+    return arr
+
+
+def nlse_dist_connect_local(solvers):
+    """Connect the slab contexts of ranks 0..n-1 of one process (virtual ranks)."""
+    _check(lib.nlse_dist_connect_local(_ctx_array(solvers), len(solvers)))
+
+
+def nlse_step_group(solvers, k: float, nsteps: int):
+    st = lib.nlse_step_group(_ctx_array(solvers), len(solvers), float(k), int(nsteps))
+    if st != NLSE_OK:
+        msgs = "; ".join(lib.nlse_last_error(sv.ctx).decode() for sv in solvers)
+        raise NLSEError(st, msgs or lib.nlse_last_error(None).decode())
+
+
+def nlse_diagnostics_group(solvers):
+    n = len(solvers)
+    m, h = (ctypes.c_double * n)(), (ctypes.c_double * n)()
+    st = lib.nlse_diagnostics_group(_ctx_array(solvers), n, m, h)
+    if st != NLSE_OK:
+        raise NLSEError(st, lib.nlse_last_error(None).decode())
+    return list(m), list(h)

@@ -15,14 +15,42 @@ def run_oracle(dims, h, psi0, k, nsteps, a=1.0, s=1.0, V=None, bc="dirichlet", s
 
 
 def run_gpu(dims, h, psi0, k, nsteps, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc", precision="fp64",
-            generic=False, chunks=None, force_dt=True):
+            generic=False, chunks=None, force_dt=True, with_info=False):
     from paper_1203_1263_b200.nlse import Solver
     with Solver(dims, h, a=a, s=s, V=V, bc=bc, scheme=scheme, precision=precision, force_dt=force_dt,
                 generic=generic) as sv:
         sv.nlse_set_psi(psi0)
         for n in (chunks or [nsteps]):
             sv.nlse_step(k, n)
-        return sv.nlse_get_psi()
+        out = sv.nlse_get_psi()
+        return (out, sv.nlse_get_info()) if with_info else out
+
+
+def run_gpu_slabs(dims, h, psi0, k, nsteps, nranks, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc",
+                  precision="fp64", generic=False, chunks=None, force_dt=True, diag=False):
+    """The same run as run_gpu, partitioned into `nranks` z slabs (virtual ranks on one GPU,
+    nlse_dist_connect_local + nlse_step_group).  Returns the gathered global Psi (and the
+    per-rank diagnostics after the run when diag=True)."""
+    from paper_1203_1263_b200 import nlse
+    svs = []
+    try:
+        for r in range(nranks):
+            z0, nl = nlse.nlse_slab_range(dims[2], nranks, r)
+            Vl = None if V is None else np.ascontiguousarray(V[z0:z0 + nl])
+            svs.append(nlse.Solver(dims, h, a=a, s=s, V=Vl, bc=bc, scheme=scheme, precision=precision,
+                                   force_dt=force_dt, generic=generic, dist=(r, nranks)))
+        nlse.nlse_dist_connect_local(svs)
+        for sv in svs:
+            sv.nlse_set_psi(np.ascontiguousarray(psi0[sv.z0:sv.z0 + sv.shape[0]]))
+        for n in (chunks or [nsteps]):
+            nlse.nlse_step_group(svs, k, n)
+        out = np.concatenate([sv.nlse_get_psi() for sv in svs], axis=0)
+        if diag:
+            return out, nlse.nlse_diagnostics_group(svs)
+        return out
+    finally:
+        for sv in svs:
+            sv.close()
 
 
 def ulp_diff(a, b, precision):

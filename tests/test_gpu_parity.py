@@ -22,13 +22,20 @@ def _k(ndim, h, scheme):
     return 0.5 * kb
 
 
-@pytest.mark.parametrize("generic", [False, True], ids=["fast", "generic"])
+@pytest.mark.parametrize("kernel", ["fast", "v1", "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 @pytest.mark.parametrize("ndim", [1, 2, 3])
-def test_matrix_bitwise(ndim, scheme, bc, precision, withV, generic):
+def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch):
+    """Every kernel family against the oracle: "fast" = the default (3D: TMA z-streaming),
+    "v1" = the cp.async z-streaming kernel (3D), "generic" = one thread per point."""
+    if kernel == "v1" and ndim != 3:
+        pytest.skip("v1 is a 3D kernel")
+    if kernel == "v1":
+        monkeypatch.setenv("NLSE_3D_KERNEL", "v1")
+    generic = kernel == "generic"
     dims = DIMS[ndim]
     h = H[ndim]
     psi0 = case_input(dims, seed=100 + ndim)
@@ -37,8 +44,12 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, generic):
     n = 12
     kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
-    got = run_gpu(dims, h, psi0, k, n, generic=generic, **kw)
-    assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV}")
+    got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
+    want = {"fast": {1: "stage1d_tile", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+            "generic": "stage_generic"}[kernel]
+    if not (kernel == "fast" and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
+        assert info["variant"] == want, info
+    assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV} {info['variant']}")
 
 
 @pytest.mark.parametrize("dims", [(3,), (4,), (3, 3), (3, 5), (5, 3), (3, 3, 3), (4, 3, 5), (3, 7, 3), (9, 3, 4)])

@@ -1,0 +1,112 @@
+"""Slab mode on one GPU with virtual ranks: the grid split into
+P z slabs, each its own context with ghost planes, remote stores into the
+neighbours' ghosts from the stage kernels and device-side neighbour barriers between
+stages (the same code path as one process per GPU, with peer pointers that happen to
+live on the same device).  The bar: bitwise identical to the single-context run, which
+is itself bitwise identical to the oracle (test_gpu_parity.py)."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import case_input, run_gpu, run_gpu_slabs, run_oracle, ulp_diff
+from paper_1203_1263_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _k(h, scheme):
+    return 0.5 * h * h / (3 * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+def test_slabs_bitwise_equal_single(scheme, bc, precision, nranks):
+    dims = (70, 37, 29)
+    psi0 = case_input(dims, seed=41)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=42))
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    k = _k(0.5, scheme)
+    one = run_gpu(dims, 0.5, psi0, k, 9, **kw)
+    many = run_gpu_slabs(dims, 0.5, psi0, k, 9, nranks, **kw)
+    assert ulp_diff(many, one, precision) == 0
+
+
+@pytest.mark.parametrize("kernel", ["v1", "generic"])
+def test_slabs_other_kernel_families(kernel, monkeypatch):
+    dims = (40, 33, 24)
+    psi0 = case_input(dims, seed=43)
+    if kernel == "v1":
+        monkeypatch.setenv("NLSE_3D_KERNEL", "v1")
+    kw = dict(s=-1.0, bc="msd", scheme="2shoc", generic=kernel == "generic")
+    k = _k(0.5, "2shoc")
+    one = run_gpu(dims, 0.5, psi0, k, 7, **kw)
+    many = run_gpu_slabs(dims, 0.5, psi0, k, 7, 4, **kw)
+    assert ulp_diff(many, one, "fp64") == 0
+
+
+def test_slabs_match_oracle_and_chunking():
+    dims = (33, 30, 26)
+    psi0 = case_input(dims, seed=44)
+    kw = dict(s=-1.0, bc="msd", scheme="2shoc")
+    k = _k(0.5, "2shoc")
+    ref = run_oracle(dims, 0.5, psi0, k, 10, **kw)
+    a = run_gpu_slabs(dims, 0.5, psi0, k, 10, 3, **kw)
+    b = run_gpu_slabs(dims, 0.5, psi0, k, 10, 3, chunks=[3, 1, 6], **kw)
+    assert ulp_diff(a, ref, "fp64") == 0
+    assert ulp_diff(b, ref, "fp64") == 0
+
+
+def test_slabs_thinnest_legal():
+    """Slabs of exactly 2w planes (the minimum), and uneven splits."""
+    for dims, P, scheme in [((20, 18, 8), 2, "2shoc"), ((20, 18, 13), 3, "2shoc"), ((20, 18, 6), 3, "cd")]:
+        psi0 = case_input(dims, seed=45)
+        kw = dict(s=-1.0, bc="msd", scheme=scheme)
+        k = _k(0.5, scheme)
+        one = run_gpu(dims, 0.5, psi0, k, 5, **kw)
+        many = run_gpu_slabs(dims, 0.5, psi0, k, 5, P, **kw)
+        assert ulp_diff(many, one, "fp64") == 0, (dims, P, scheme)
+
+
+def test_slab_diagnostics_are_global():
+    import oracle
+    dims = (36, 28, 31)
+    psi0 = case_input(dims, seed=46)
+    V = np.abs(inputs.random_smooth(dims, seed=47))
+    out, (m, h) = run_gpu_slabs(dims, 0.25, psi0, 0.001, 3, 4, s=-1.0, V=V, bc="msd", diag=True)
+    p = oracle.Problem(dims, 0.25, a=1.0, s=-1.0, bc="msd")
+    mo, ho = oracle.diagnostics(p, out, V)
+    assert len(set(m)) == 1 and len(set(h)) == 1        # every rank holds the same global sums
+    assert abs(m[0] - mo) <= 1e-12 * abs(mo) and abs(h[0] - ho) <= 1e-12 * abs(ho)
+
+
+def test_slab_errors():
+    from paper_1203_1263_b200.nlse import NLSE_ERR_ARG, NLSE_ERR_COMM, NLSEError, Solver
+    with pytest.raises(NLSEError) as e:
+        Solver((20, 20, 7), 0.5, scheme="2shoc", dist=(1, 2))       # 4 + 3 planes: 3 < 2w
+    assert e.value.status == NLSE_ERR_ARG
+    with pytest.raises(NLSEError) as e:
+        Solver((20, 20), 0.5, dist=(0, 2))                          # 2D is not partitioned
+    assert e.value.status == NLSE_ERR_ARG
+    sv = Solver((20, 20, 16), 0.5, dist=(1, 2))
+    with pytest.raises(NLSEError) as e:
+        sv.nlse_step(0.001, 1)                                       # not connected yet
+    assert e.value.status == NLSE_ERR_COMM
+    sv.close()
+
+
+def test_virtual_group_requires_group_calls():
+    from paper_1203_1263_b200 import nlse
+    svs = [nlse.Solver((16, 16, 12), 0.5, s=-1.0, bc="msd", dist=(r, 2)) for r in range(2)]
+    try:
+        nlse.nlse_dist_connect_local(svs)
+        with pytest.raises(nlse.NLSEError) as e:
+            svs[0].nlse_step(0.001, 1)
+        assert e.value.status == nlse.NLSE_ERR_ARG
+        with pytest.raises(nlse.NLSEError):
+            svs[1].nlse_diagnostics()
+    finally:
+        for sv in svs:
+            sv.close()
