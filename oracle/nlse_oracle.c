@@ -20,7 +20,7 @@ static int oracle_check(const oracle_problem *p)
         else if (p->n[d] != 1) return -1;
     }
     if (!(p->h > 0) || !(p->a > 0) || !isfinite(p->s)) return -1;
-    if (p->bc != 0 && p->bc != 1) return -1;
+    if (p->bc != 0 && p->bc != 1 && p->bc != 2) return -1;
     if (p->order != 2 && p->order != 4) return -1;
     return 0;
 }

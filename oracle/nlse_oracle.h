@@ -28,7 +28,7 @@ typedef struct {
     double h;       /* grid spacing, same in every direction */
     double a;       /* dispersion coefficient, a > 0 */
     double s;       /* nonlinearity coefficient */
-    int bc;         /* 0 = Dirichlet, 1 = MSD */
+    int bc;         /* 0 = Dirichlet, 1 = MSD, 2 = L0 */
     int order;      /* 2 = CD, 4 = 2SHOC */
 } oracle_problem;
 

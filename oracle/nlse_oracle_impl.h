@@ -119,6 +119,7 @@ static REAL FN(nlin)(const FN(oracle_consts) *c, const REAL *V, long q, REAL yr,
  *   MSD      (BCMSDlap) P:336-344: Lap Psi_b = [Im(i Lap Psi_{b-1}/Psi_{b-1})
  *                                     + (N_{b-1} - N_b)/a] Psi_b
  *     with Im(i z) = Re z (reading R-MSD-LAP), and Lap Psi_{b-1} = D_{b-1}.
+ *   L0       (BCL0lap) P:352-355:  Lap Psi_b = 0 ("by definition").
  * Only boundary points with exactly one boundary axis (faces) are reachable
  * from 2SHOC step 2 at an interior point; edges and corners are set to NaN so
  * that any use poisons the result (reading R-DFACE).
@@ -134,6 +135,7 @@ static void FN(d_boundary)(const oracle_problem *p, const FN(oracle_consts) *c, 
                 if (m == 0) continue;
                 long q = (k * ny + j) * nx + i;
                 if (m > 1) { dr[q] = (REAL)NAN; di[q] = (REAL)NAN; continue; }
+                if (p->bc == 2) { dr[q] = 0; di[q] = 0; continue; }
                 REAL nb = FN(nlin)(c, V, q, yr[q], yi[q]);
                 if (p->bc == 0) {
                     REAL t = c->inv_a * nb;
@@ -227,8 +229,10 @@ static void FN(f_point)(const FN(oracle_consts) *c, REAL yr, REAL yi, REAL lr, R
  *   MSD (msd) P:331-335: dPsi_b/dt = i Im[(1/Psi_{b-1}) dPsi_{b-1}/dt] Psi_b,
  *     dPsi_{b-1}/dt "precomputed using the internal finite-difference scheme"
  *     -- so this runs after the interior F.
- *   Im[F/Y] = (F^I Y^R - F^R Y^I)/|Y|^2. */
-static void FN(f_boundary)(const oracle_problem *p, const FN(oracle_consts) *c,
+ *   Im[F/Y] = (F^I Y^R - F^R Y^I)/|Y|^2.
+ *   L0 (BCL0dt) P:347-350: dPsi_b/dt = i(s|Psi_b|^2 - V_b) Psi_b, evaluated as
+ *     (fsplit) with Lap Psi_b = 0 ((BCL0lap) P:352-355; reading R-L0). */
+static void FN(f_boundary)(const oracle_problem *p, const FN(oracle_consts) *c, const REAL *V,
                            const REAL *yr, const REAL *yi, REAL *fr, REAL *fi)
 {
     const long nx = p->n[0], ny = p->n[1], nz = p->n[2];
@@ -238,6 +242,7 @@ static void FN(f_boundary)(const oracle_problem *p, const FN(oracle_consts) *c,
                 if (FN(n_bnd_axes)(p, i, j, k) == 0) continue;
                 long q = (k * ny + j) * nx + i;
                 if (p->bc == 0) { fr[q] = 0; fi[q] = 0; continue; }
+                if (p->bc == 2) { FN(f_point)(c, yr[q], yi[q], 0, 0, V, q, &fr[q], &fi[q]); continue; }
                 long b1 = FN(inward)(p, i, j, k);
                 REAL rho1 = (yr[b1] * yr[b1]) + (yi[b1] * yi[b1]);
                 REAL m = 0;
@@ -276,7 +281,7 @@ static void FN(rhs)(const oracle_problem *p, const FN(oracle_consts) *c, const R
                 long q = (k * ny + j) * nx + i;
                 FN(f_point)(c, yr[q], yi[q], lr[q], li[q], V, q, &fr[q], &fi[q]);
             }
-    FN(f_boundary)(p, c, yr, yi, fr, fi);
+    FN(f_boundary)(p, c, V, yr, yi, fr, fi);
 }
 
 int FN(oracle_rhs)(const oracle_problem *p, const REAL *V, const REAL *yr, const REAL *yi,

@@ -41,7 +41,7 @@ class _Problem(ctypes.Structure):
                 ("order", ctypes.c_int)]
 
 
-BC = {"dirichlet": 0, "msd": 1}
+BC = {"dirichlet": 0, "msd": 1, "l0": 2}
 ORDER = {"cd": 2, "2shoc": 4}
 
 
@@ -51,7 +51,7 @@ class Problem:
     h: float
     a: float = 1.0
     s: float = 1.0
-    bc: str = "dirichlet"  # "dirichlet" | "msd"
+    bc: str = "dirichlet"  # "dirichlet" | "msd" | "l0"
     scheme: str = "2shoc"  # "cd" | "2shoc"
     precision: str = "fp64"  # "fp64" | "fp32"
 

@@ -1,14 +1,142 @@
-// tile2d.cuh -- 1D / 2D interior stage kernels (placeholder: interior-only generic evaluation).
+// tile2d.cuh -- 2D interior stage kernel (§8(a) rows a1-a5, a7 for 2D grids).
+//
+// CTA = 256 threads owns a TX x TY = 32 x 16 tile of output points (each thread two
+// rows, ty and ty + 8).  The stage input Y is staged once per stage in shared memory
+// as a (TX+2H) x (TY+2H) tile with an H = w wide halo (coalesced 16-byte loads, one
+// warp per tile row); for 2SHOC, step 1 (D = Delta_2 Y / h^2, (2d2shocs1) P:202-210)
+// is evaluated once per tile point plus a one-point ring into a shared D tile (faces:
+// the Laplacian form of the BC; D never touches HBM); step 2
+// ((2d2shocs2) P:214-228), F (fsplit) and the RK4 stage combine then run per owned
+// point with Psi, K_tot, V read once from HBM.  The grid working set of the 2D configs
+// (1024^2 fp64 + V: 75 MB) is L2-resident on B200, so the halo re-reads are L2 hits.
+// Domain-boundary outputs come from stage_boundary.  DAG: DESIGN.md §3.1 (bitwise =
+// oracle).
 #pragma once
-#include "stream3d.cuh"
+#include "generic.cuh"
 
 namespace nlse {
 
+constexpr int T2_TX = 32, T2_TY = 16, T2_NT = 256;
+
+template <typename T, int ORDER, int BC, int STAGE>
+__global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
+    using C = cplx<T>;
+    constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
+    constexpr int PX = T2_TX + 2 * H, PY = T2_TY + 2 * H;
+    constexpr int DPX = T2_TX + 2, DPY = T2_TY + 2;
+    __shared__ C ys[PY * PX];
+    __shared__ C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
+    const int nx = int(A.g.nx), ny = int(A.g.ny);
+    const int x0 = blockIdx.x * T2_TX, y0 = blockIdx.y * T2_TY;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+
+    // (1) Y tile with halo (zero outside the grid; those values are never used)
+    for (int ly = ty - H; ly < T2_TY + H; ly += T2_NT / 32) {
+        const int gy = y0 + ly;
+        for (int lx = tx - H; lx < T2_TX + H; lx += 32) {
+            const int gx = x0 + lx;
+            C v; v.x = T(0); v.y = T(0);
+            if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) v = __ldg(A.Y + int64_t(gy) * A.g.sy + gx);
+            ys[(ly + H) * PX + (lx + H)] = v;
+        }
+    }
+    __syncthreads();
+    auto Ys = [&](int lx, int ly) -> C { return ys[(ly + H) * PX + (lx + H)]; };
+    auto D_int = [&](int lx, int ly) -> C {
+        const C yc = Ys(lx, ly);
+        const C y2 = cadd(yc, yc);
+        C acc = csub(cadd(Ys(lx - 1, ly), Ys(lx + 1, ly)), y2);
+        acc = cadd(acc, csub(cadd(Ys(lx, ly - 1), Ys(lx, ly + 1)), y2));
+        return cscale(A.c.ih2, acc);
+    };
+    auto nlin = [&](int gx, int gy, C yq) -> T {
+        T rho = (yq.x * yq.x) + (yq.y * yq.y);
+        T n = A.c.s * rho;
+        if (A.V) n = n - __ldg(A.V + int64_t(gy) * A.g.sy + gx);
+        return n;
+    };
+
+    // (2) 2SHOC step 1 over the tile + ring
+    if (ORDER == ORDER_2SHOC) {
+        for (int e = tid; e < DPX * DPY; e += T2_NT) {
+            const int lx = e % DPX - 1, ly = e / DPX - 1;
+            const int gx = x0 + lx, gy = y0 + ly;
+            C d; d.x = T(NAN); d.y = T(NAN);
+            if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
+                const bool fx = (gx == 0 || gx == nx - 1), fy = (gy == 0 || gy == ny - 1);
+                if (!fx && !fy) {
+                    d = D_int(lx, ly);
+                } else if (!(fx && fy)) {
+                    // face: Laplacian form of the BC with b' the in-plane inward neighbour
+                    const C yb = Ys(lx, ly);
+                    const T nb = nlin(gx, gy, yb);
+                    if (BC == BC_DIRICHLET) {
+                        const T t = A.c.inv_a * nb;
+                        d.x = -(t * yb.x); d.y = -(t * yb.y);
+                    } else {
+                        int lx1 = lx, ly1 = ly;
+                        if (gx == 0) lx1 = lx + 1; else if (gx == nx - 1) lx1 = lx - 1;
+                        else if (gy == 0) ly1 = ly + 1; else ly1 = ly - 1;
+                        const C y1 = Ys(lx1, ly1), d1 = D_int(lx1, ly1);
+                        const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+                        T re = T(0);
+                        if (!(rho1 < A.c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+                        const T n1 = nlin(x0 + lx1, y0 + ly1, y1);
+                        const T gg = re + ((n1 - nb) * A.c.inv_a);
+                        d = cscale(gg, yb);
+                    }
+                }
+            }
+            ds[e] = d;
+        }
+        __syncthreads();
+    }
+
+    // (3) step 2, F, RK4 stage combine at the owned interior points
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const int lx = tx, ly = ty + 8 * r;
+        const int gx = x0 + lx, gy = y0 + ly;
+        if (gx < 1 || gx > nx - 2 || gy < 1 || gy > ny - 2) continue;
+        const int64_t q = int64_t(gy) * A.g.sy + gx;
+        const C yc = Ys(lx, ly);
+        C L;
+        if (ORDER == ORDER_CD) {
+            L = D_int(lx, ly);
+        } else {
+            const C y4 = cscale(T(4), yc);
+            const C pxa = cadd(Ys(lx - 1, ly - 1), Ys(lx + 1, ly - 1));
+            const C pxb = cadd(Ys(lx - 1, ly + 1), Ys(lx + 1, ly + 1));
+            const C cxy = csub(cadd(pxa, pxb), y4);
+            const C *Dp = ds + (ly + 1) * DPX + (lx + 1);
+            const C sd = cadd(cadd(Dp[-1], Dp[1]), cadd(Dp[-DPX], Dp[DPX]));
+            const C td = csub(sd, cscale(T(12), Dp[0]));
+            L = csub(cscale(A.c.c16h2, cxy), cscale(A.c.c112, td));
+        }
+        // F (fsplit) P:424-428
+        const T rho = (yc.x * yc.x) + (yc.y * yc.y);
+        const T sr = A.c.s * rho;
+        T fr = (-(A.c.a * L.y)) - (sr * yc.y);
+        T fi = (A.c.a * L.x) + (sr * yc.x);
+        if (A.V) {
+            const T v = __ldg(A.V + q);
+            fr = fr + (v * yc.y);
+            fi = fi - (v * yc.x);
+        }
+        C F; F.x = fr; F.y = fi;
+        const C psi = (STAGE == 1) ? yc : A.Psi[q];
+        rk_combine<STAGE, T>(A, q, 0, F, psi);
+    }
+}
+
 template <typename T, int ORDER, int BC, int STAGE>
 void launch_tile2d(const StageArgs<T> &A, cudaStream_t st) {
-    const int64_t m = (A.g.nx - 2) * (A.g.ny - 2);
-    stage_interior_generic<T, 2, ORDER, BC, STAGE><<<unsigned((m + 255) / 256), 256, 0, st>>>(A);
+    const dim3 grid(unsigned((A.g.nx + T2_TX - 1) / T2_TX), unsigned((A.g.ny + T2_TY - 1) / T2_TY));
+    stage2d_tile<T, ORDER, BC, STAGE><<<grid, T2_NT, 0, st>>>(A);
 }
+
+// 1D: interior points, one thread per point (the 1D configs are latency-bound: 1025-2001
+// points per stage).
 template <typename T, int ORDER, int BC, int STAGE>
 void launch_tile1d(const StageArgs<T> &A, cudaStream_t st) {
     const int64_t m = A.g.nx - 2;

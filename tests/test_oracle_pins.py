@@ -20,6 +20,11 @@ def interior(ndim, margin=1):
     return (s,) * ndim
 
 
+def case_field(dims, seed):
+    """Seeded smooth complex field with a background of modulus ~1."""
+    return inputs.random_smooth(tuple(dims), seed=seed, modes=5, amp=0.4, offset=1.0)
+
+
 # ---------------------------------------------------------------------------------------------
 # Stencils (2SHOC step 1 / CD, 2SHOC step 2) -- closed forms
 # ---------------------------------------------------------------------------------------------
@@ -436,3 +441,67 @@ def test_diagnostics_gaussian_closed_forms(oracle_lib, a, s, w):
     assert abs(M - math.pi * sig ** 2) < 1e-10
     Hx = a * (math.pi + kap ** 2 * math.pi * sig ** 2) + w * w * math.pi * sig ** 4 - 0.5 * s * math.pi * sig ** 2 / 2
     assert abs(H - Hx) < 2e-3 * max(1.0, abs(Hx)), (H, Hx)
+
+
+# ---------------------------------------------------------------- L0 boundary condition (§8(f) rank 1)
+
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_l0_uniform_field_is_the_scalar_ode(oracle_lib, ndim):
+    """L0 ((BCL0dt) P:347-350, (BCL0lap) P:352-355): a uniform field has Lap = 0 inside and,
+    by definition, on the boundary, so every point -- boundary included -- follows the scalar
+    RK4 of z' = i(s|z|^2 - V0) z bit for bit."""
+    dims = (7, 5, 6)[:ndim]
+    s, V0, k, n = 1.7, 0.3, 0.01, 30
+    z = 0.6 + 0.7j
+    psi = np.full(tuple(reversed(dims)), z)
+    p = Problem(dims, 0.5, a=1.0, s=s, bc="l0", scheme="2shoc")
+    out = oracle.step(p, psi, k, n, np.full(psi.shape, V0))
+
+    def f(w):
+        return 1j * (s * abs(w) ** 2 - V0) * w
+    for _ in range(n):
+        k1 = f(z); k2 = f(z + k / 2 * k1); k3 = f(z + k / 2 * k2); k4 = f(z + k * k3)
+        z = z + k / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+    assert np.ptp(out.real) == 0 and np.ptp(out.imag) == 0
+    assert abs(out.flat[0] - z) < 1e-14
+
+
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_l0_boundary_points_decouple(oracle_lib, ndim, scheme):
+    """Under L0 the boundary F depends on Psi_b only: with s = 0 and V = V0 every boundary
+    point is multiplied per step by the RK4 polynomial of -i V0 k, whatever the interior does."""
+    dims = (9, 8, 7)[:ndim]
+    psi = case_field(dims, 71)
+    V0, k, n = 1.3, 0.004, 12
+    p = Problem(dims, 0.3, a=0.8, s=0.0, bc="l0", scheme=scheme)
+    out = oracle.step(p, psi, k, n, np.full(psi.shape, V0))
+    zz = -1j * V0 * k
+    g = (1 + zz + zz ** 2 / 2 + zz ** 3 / 6 + zz ** 4 / 24) ** n
+    bnd = ~np.pad(np.ones(tuple(d - 2 for d in reversed(dims)), bool), 1)
+    np.testing.assert_allclose(out[bnd], psi[bnd] * g, rtol=1e-14, atol=0)
+    assert not np.allclose(out[~bnd], psi[~bnd] * g)        # the interior does feel the Laplacian
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_l0_bc_forms_consistent(oracle_lib, precision):
+    """F_b from the Laplacian form (fsplit with Lap = 0) equals the time-derivative form
+    i(s|Psi_b|^2 - V_b)Psi_b (evaluated here in numpy complex arithmetic) to a few ulps; D_b = 0
+    exactly on faces (2SHOC step 1 boundary values), NaN on edges / corners (R-DFACE)."""
+    dims = (8, 7, 6)
+    psi = case_field(dims, 72)
+    V = np.abs(case_field(dims, 73))
+    p = Problem(dims, 0.3, a=0.9, s=-1.2, bc="l0", scheme="2shoc", precision=precision)
+    F = oracle.rhs(p, psi, V)
+    T = np.float64 if precision == "fp64" else np.float32
+    ps = psi.astype(np.complex128 if precision == "fp64" else np.complex64)
+    Vt = V.astype(T)
+    want = 1j * (T(-1.2) * np.abs(ps) ** 2 - Vt) * ps
+    bnd = ~np.pad(np.ones(tuple(d - 2 for d in reversed(dims)), bool), 1)
+    eps = np.finfo(T).eps
+    assert np.all(np.abs(F[bnd] - want[bnd]) <= 8 * eps * (np.abs(want[bnd]) + np.abs(ps[bnd])))
+    D, _ = oracle.laplacian(p, psi, V)
+    nb = sum(((np.arange(n) == 0) | (np.arange(n) == n - 1)).astype(int).reshape(
+        [-1 if a == ax else 1 for a in range(3)]) for ax, n in enumerate(reversed(dims)))
+    assert np.all(D[nb == 1] == 0)
+    assert np.all(np.isnan(D[nb >= 2]))
