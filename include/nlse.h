@@ -53,8 +53,10 @@ typedef enum {
  *   DIRICHLET: Psi_b = B fixed (BCDdef) P:310-313, dPsi_b/dt = 0 (BCDdt) P:315-318,
  *              Laplacian form (BCDlap) P:320-323 for 2SHOC.
  *   MSD:       |Psi_b|^2 = B fixed (BCMSDdef) P:326-329, time-derivative form (msd)
- *              P:331-335, Laplacian form (BCMSDlap) P:336-344.                      */
-typedef enum { NLSE_BC_DIRICHLET = 0, NLSE_BC_MSD = 1 } nlse_bc;
+ *              P:331-335, Laplacian form (BCMSDlap) P:336-344.
+ *   L0:        Laplacian zero: dPsi_b/dt = i(s|Psi_b|^2 - V_b)Psi_b (BCL0dt) P:347-350,
+ *              Lap Psi_b = 0 (BCL0lap) P:352-355 (reading R-L0).            */
+typedef enum { NLSE_BC_DIRICHLET = 0, NLSE_BC_MSD = 1, NLSE_BC_L0 = 2 } nlse_bc;
 
 /* Laplacian: CD = 2nd-order central differences; 2SHOC = the 4th-order
  * two-step compact scheme (2shoc1d)-(3d2shocs2) P:195-299.                          */

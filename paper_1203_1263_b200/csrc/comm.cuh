@@ -25,16 +25,18 @@ constexpr int MAX_RANKS = 16;
 struct CommBlock {
     unsigned long long flags[MAX_RANKS];
     double xbuf[MAX_RANKS][2];
+    unsigned long long my_epoch;   // this rank's barrier count (written by its own launches only)
 };
 
-// Barrier arguments: signal `epoch` into sig[i]->flags[me] for every listed peer, then
-// wait until own->flags[w] >= epoch for every listed waiter rank w.
+// Barrier arguments: signal the next epoch into sig[i]->flags[me] for every listed peer,
+// then wait until own->flags[w] >= epoch for every listed waiter rank w.  The epoch
+// counter lives in the rank's own comm block (advanced by the signalling launch), so
+// the launch parameters are the same every step and a captured CUDA graph can replay.
 struct BarrierArgs {
     CommBlock *own;
     CommBlock *sig[MAX_RANKS];
     int wait_rank[MAX_RANKS];
     int nsig, nwait, me;
-    unsigned long long epoch;
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
@@ -51,15 +53,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // (a spinning kernel must never sit in front of the work that releases it).
 __global__ void __launch_bounds__(32) peer_barrier(BarrierArgs b, int mode) {
     const int t = threadIdx.x;
+    const unsigned long long epoch = b.own->my_epoch + ((mode & 1) ? 1ull : 0ull);
+    __syncwarp();
+    if ((mode & 1) && t == 0) b.own->my_epoch = epoch;
     if ((mode & 1) && t < b.nsig) {
         __threadfence_system();
-        st_release_sys(&b.sig[t]->flags[b.me], b.epoch);
+        st_release_sys(&b.sig[t]->flags[b.me], epoch);
     }
     if ((mode & 2) && t < b.nwait) {
         const unsigned long long *f = &b.own->flags[b.wait_rank[t]];
-        while (ld_acquire_sys(f) < b.epoch) __nanosleep(64);
+        while (ld_acquire_sys(f) < epoch) __nanosleep(64);
     }
     __syncwarp();
+}
+
+// Advance the device step counter after a launch sequence of n steps.
+__global__ void add_steps(int *counter, int n) {
+    if (threadIdx.x == 0) *counter += n;
 }
 
 // Push this rank's (mass, energy) partial pair into every rank's xbuf[me].

@@ -11,7 +11,7 @@
 
 namespace nlse {
 
-enum BcKind { BC_DIRICHLET = 0, BC_MSD = 1 };
+enum BcKind { BC_DIRICHLET = 0, BC_MSD = 1, BC_L0 = 2 };
 enum OrderKind { ORDER_CD = 2, ORDER_2SHOC = 4 };
 
 template <typename T> struct Vec2;
@@ -68,7 +68,9 @@ template <typename T> struct StageArgs {
     Grid g;
     Consts<T> c;
     int *diverged;        // stage 4: atomicMin(step index) when a non-finite value is produced
-    int step;             // absolute step index (for the divergence report)
+    const int *step_base; // device counter of the steps completed before this launch sequence
+    int step;             // step index within the launch sequence (absolute = *step_base + step;
+                          // read only when a non-finite value appears, so CUDA graphs can replay)
     // Slab mode: the stage output of the first / last `wsend` owned planes is also stored
     // into the lower / upper neighbour's ghost planes (remote stores over NVLink, the halo
     // exchange a9 fused into the producing kernel).  peer_lo[q] / peer_hi[q] address the
@@ -106,7 +108,7 @@ __device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, int
         C k = A.K[q];
         C r = cadd(psi, cscale(A.c.kc, cadd(k, F)));
         store_out(A, q, kz, r);
-        if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(A.diverged, A.step);
+        if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(A.diverged, *A.step_base + A.step);
     }
 }
 

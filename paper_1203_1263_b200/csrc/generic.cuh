@@ -63,6 +63,7 @@ struct PointEval {
     __device__ __forceinline__ C D_face(int64_t i, int64_t j, int64_t k) const {
         const int64_t q = idx(i, j, k);
         const C yb = y(q);
+        if (BC == BC_L0) { C z; z.x = T(0); z.y = T(0); return z; }   // (BCL0lap) P:352-355
         const T nb = nlin(q, yb);
         if (BC == BC_DIRICHLET) {
             T t = c.inv_a * nb;
@@ -134,10 +135,16 @@ struct PointEval {
         return F_from(q, y(q), L_int(i, j, k));
     }
 
-    // F at a boundary point: (BCDdt) P:315-318 / (msd) P:331-335.
+    // F at a boundary point: (BCDdt) P:315-318 / (msd) P:331-335 / (BCL0dt) P:347-350
+    // evaluated as (fsplit) with Lap Psi_b = 0 (reading R-L0).
     __device__ __forceinline__ C F_bnd(int64_t i, int64_t j, int64_t k) const {
         C f;
         if (BC == BC_DIRICHLET) { f.x = T(0); f.y = T(0); return f; }
+        if (BC == BC_L0) {
+            const int64_t qb = idx(i, j, k);
+            C zero; zero.x = T(0); zero.y = T(0);
+            return F_from(qb, y(qb), zero);
+        }
         int64_t i1 = i, j1 = j, k1 = k;
         inward(i1, j1, k1);
         const int64_t q1 = idx(i1, j1, k1);

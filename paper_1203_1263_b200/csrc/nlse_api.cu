@@ -39,6 +39,7 @@ static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
 struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
 
 constexpr int TMA_P = 2;        // TMA ring prefetch depth (planes ahead)
+constexpr int GRAPH_STEPS = 8;  // RK4 steps per captured CUDA graph
 
 enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2 };
 
@@ -76,6 +77,10 @@ struct nlse_ctx {
     void *K = nullptr, *V = nullptr;
     int *d_div = nullptr;
     int *h_div = nullptr;            // pinned
+    int *d_steps = nullptr;          // device counter of completed steps (divergence report)
+    // CUDA graph of GRAPH_STEPS steps for the current k (nlse_step with many steps)
+    cudaGraphExec_t graph_exec = nullptr;
+    double graph_k = 0;
     double *d_partial = nullptr, *d_result = nullptr, *h_result = nullptr;
     int diag_blocks = 0;
     cudaStream_t stream = nullptr;
@@ -104,7 +109,6 @@ struct nlse_ctx {
     int64_t peer_nloc[2] = {0, 0};
     CommBlock *peer_comm[MAX_RANKS] = {nullptr};
     std::vector<void *> ipc_opened;
-    unsigned long long epoch = 0;
     bool ghost_stale = false;
     bool virtual_group = false;      // connected by nlse_dist_connect_local: _group calls only
 };
@@ -306,6 +310,7 @@ void enqueue_stage_t(nlse_ctx *c, int stage, double k, int step) {
     A.g = c->g;
     A.c = make_consts<T>(c, kc);
     A.diverged = c->d_div;
+    A.step_base = c->d_steps;
     A.step = step;
     peer_ptrs<T>(c, obuf_of_stage(stage), A.peer_lo, A.peer_hi);
     A.wsend = halo_w(c);
@@ -322,6 +327,7 @@ template <typename F>
 auto dispatch(nlse_ctx *c, F &&f) {
     auto by_bc = [&](auto T, auto DIM, auto ORD) {
         if (c->bc == NLSE_BC_MSD) return f(T, DIM, ORD, std::integral_constant<int, BC_MSD>());
+        if (c->bc == NLSE_BC_L0) return f(T, DIM, ORD, std::integral_constant<int, BC_L0>());
         return f(T, DIM, ORD, std::integral_constant<int, BC_DIRICHLET>());
     };
     auto by_order = [&](auto T, auto DIM) {
@@ -355,8 +361,6 @@ void enqueue_barrier(nlse_ctx *c, bool full, int mode = 3) {
     BarrierArgs b{};
     b.own = c->comm;
     b.me = c->rank;
-    if (mode & 1) ++c->epoch;
-    b.epoch = c->epoch;
     for (int j = 0; j < c->nranks; j++) {
         if (j == c->rank) continue;
         if (!full && j != c->rank - 1 && j != c->rank + 1) continue;
@@ -409,12 +413,53 @@ nlse_status check_step_args(nlse_ctx *c, double k, int64_t nsteps) {
     return NLSE_OK;
 }
 
-// Enqueue one RK4 stage, followed (slab mode) by the neighbour barrier (mode as
-// enqueue_barrier).
+// Enqueue one RK4 stage of step n of the current launch sequence, followed (slab mode)
+// by the neighbour barrier (mode as enqueue_barrier).
 void enqueue_step_stage(nlse_ctx *c, int stage, double k, int64_t n, int mode = 3) {
-    const int step = int(std::min<int64_t>(c->steps_done + n, INT32_MAX - 1));
-    enqueue_stage(c, stage, k, step);
+    enqueue_stage(c, stage, k, int(std::min<int64_t>(n, INT32_MAX / 2)));
     enqueue_barrier(c, false, mode);
+}
+
+void enqueue_add_steps(nlse_ctx *c, int64_t n) {
+    add_steps<<<1, 1, 0, c->stream>>>(c->d_steps, int(n));
+}
+
+void drop_graph(nlse_ctx *c) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+}
+
+// Capture GRAPH_STEPS steps (all launches, barriers and the step-counter update) once
+// per k; false if capture is unavailable (then the caller launches directly).
+bool ensure_graph(nlse_ctx *c, double k) {
+    if (c->graph_exec && c->graph_k == k) return true;
+    drop_graph(c);
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    for (int n = 0; n < GRAPH_STEPS; n++)
+        for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+    enqueue_add_steps(c, GRAPH_STEPS);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->graph_exec = nullptr;
+        return false;
+    }
+    c->graph_k = k;
+    return true;
+}
+
+bool graphs_enabled(const nlse_ctx *c, int64_t nsteps) {
+    static const bool env_off = [] {
+        const char *e = getenv("NLSE_GRAPHS");
+        return e && e[0] == '0';
+    }();
+    return !env_off && !c->timing && !c->virtual_group && nsteps >= 2 * GRAPH_STEPS;
 }
 
 nlse_status finish_steps(nlse_ctx *c, int64_t nsteps) {
@@ -553,7 +598,7 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     if (!(h > 0) || !std::isfinite(h)) return fail(nullptr, NLSE_ERR_ARG, "h must be finite and > 0");
     if (!(a > 0) || !std::isfinite(a)) return fail(nullptr, NLSE_ERR_ARG, "a must be finite and > 0");
     if (!std::isfinite(s)) return fail(nullptr, NLSE_ERR_ARG, "s must be finite");
-    if (bc != NLSE_BC_DIRICHLET && bc != NLSE_BC_MSD) return fail(nullptr, NLSE_ERR_ARG, "unknown bc");
+    if (bc != NLSE_BC_DIRICHLET && bc != NLSE_BC_MSD && bc != NLSE_BC_L0) return fail(nullptr, NLSE_ERR_ARG, "unknown bc");
     if (order != NLSE_CD2 && order != NLSE_2SHOC4) return fail(nullptr, NLSE_ERR_ARG, "unknown order");
     if (prec != NLSE_FP32 && prec != NLSE_FP64) return fail(nullptr, NLSE_ERR_ARG, "unknown precision");
     const int w = order == NLSE_2SHOC4 ? 2 : 1;
@@ -629,6 +674,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         CREATE_TRY(cudaMalloc(&c->comm, sizeof(CommBlock)));
         CREATE_TRY(cudaMemsetAsync(c->comm, 0, sizeof(CommBlock), c->stream));
     }
+    CREATE_TRY(cudaMalloc(&c->d_steps, sizeof(int)));
+    CREATE_TRY(cudaMemsetAsync(c->d_steps, 0, sizeof(int), c->stream));
     CREATE_TRY(cudaMalloc(&c->d_div, sizeof(int)));
     CREATE_TRY(cudaMallocHost(&c->h_div, sizeof(int)));
     int big = INT32_MAX;
@@ -706,7 +753,8 @@ void nlse_destroy(nlse_ctx *c) {
     for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     for (int b = 0; b < 3; b++) cudaFree(c->alloc[b]);
     cudaFree(c->K); cudaFree(c->V); cudaFree(c->comm);
-    cudaFree(c->d_div); cudaFree(c->d_partial); cudaFree(c->d_result);
+    drop_graph(c);
+    cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result);
     if (c->h_div) cudaFreeHost(c->h_div);
     if (c->h_result) cudaFreeHost(c->h_result);
     c->stream_ref.reset();    // destroys the stream with its last user
@@ -846,8 +894,16 @@ nlse_status nlse_step(nlse_ctx *c, double k, int64_t nsteps) {
     if ((st = check_step_args(c, k, nsteps))) return st;
     if (nsteps == 0) return NLSE_OK;
     if ((st = enqueue_halo_refresh(c))) return st;
-    for (int64_t n = 0; n < nsteps; n++)
-        for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+    int64_t done = 0;
+    if (graphs_enabled(c, nsteps) && ensure_graph(c, k)) {
+        for (; done + GRAPH_STEPS <= nsteps; done += GRAPH_STEPS)
+            CUDA_TRY(c, cudaGraphLaunch(c->graph_exec, c->stream));
+    }
+    if (done < nsteps) {
+        for (int64_t n = 0; n < nsteps - done; n++)
+            for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+        enqueue_add_steps(c, nsteps - done);
+    }
     return finish_steps(c, nsteps);
 }
 
@@ -870,6 +926,7 @@ nlse_status nlse_step_group(nlse_ctx *const *ctxs, int n, double k, int64_t nste
             for (int j = 0; j < n; j++) enqueue_step_stage(ctxs[j], s, k, t, 1);
             for (int j = 0; j < n; j++) enqueue_barrier(ctxs[j], false, 2);
         }
+    for (int j = 0; j < n; j++) enqueue_add_steps(ctxs[j], nsteps);
     nlse_status first = NLSE_OK;
     for (int j = 0; j < n; j++) {
         nlse_status st = finish_steps(ctxs[j], nsteps);

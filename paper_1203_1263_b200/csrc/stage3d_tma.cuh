@@ -26,6 +26,7 @@
 // follows the DAG of DESIGN.md §3.1, so the output is bit-identical to the oracle.
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include "generic.cuh"
 
 namespace nlse {
@@ -67,10 +68,17 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap *map
 template <typename T, int ORDER, int P>
 struct T3Cfg {
     static constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
+    // x halo of the staged tile: a TMA box must start on a 16-byte boundary, so fp32 tiles
+    // carry a 2-point x halo even for CD (x0 is a multiple of 32)
+    static constexpr int HX = (sizeof(T) == 4) ? 2 : H;
     static constexpr int TX = 32, TY = 8, NT = TX * TY;
-    static constexpr int PX = TX + 2 * H, PY = TY + 2 * H;
+    static constexpr int PX = TX + 2 * HX, PY = TY + 2 * H;
     static constexpr int CB = 2 * int(sizeof(T));                   // bytes per complex value
-    static constexpr int NS = P + 4, NP = P + 2, ND = (ORDER == ORDER_2SHOC) ? 3 : 0;
+    // Psi/K/V prefetch depth (planes ahead); Y uses P.  A slot is refilled only after every
+    // thread has finished the plane three planes back (see the barrier protocol in t3_run),
+    // hence ring sizes P + 5 (Y: planes z..z+2 in use) and PP + 3.
+    static constexpr int PP = (sizeof(T) == 8) ? 1 : 2;
+    static constexpr int NS = P + 5, NP = PP + 3, ND = (ORDER == ORDER_2SHOC) ? 4 : 0;
     static constexpr int DPX = TX + 2, DPY = TY + 2;
     static constexpr int up128(int b) { return (b + 127) / 128 * 128; }
     static constexpr int YBYTES = PX * PY * CB;
@@ -81,7 +89,7 @@ struct T3Cfg {
     static constexpr int OFF_PKV = NS * YSLOT;
     static constexpr int OFF_D = OFF_PKV + NP * PKVSLOT;
     static constexpr int OFF_BAR = OFF_D + ND * DSLOT;
-    static constexpr int SMEM = OFF_BAR + (NS + NP) * 8;
+    static constexpr int SMEM = OFF_BAR + (NS + NP + 2) * 8;   // + two CTA barriers
     // box dimensions (in T elements along x) of the four tensor maps
     static constexpr int BOX_Y_X = 2 * PX, BOX_Y_Y = PY;
     static constexpr int BOX_C_X = 2 * TX, BOX_R_X = TX, BOX_O_Y = TY;
@@ -99,14 +107,14 @@ template <typename T, int ORDER, int BC, int STAGE, int P, bool EDGE>
 struct T3Body {
     using C = cplx<T>;
     using Cfg = T3Cfg<T, ORDER, P>;
-    static constexpr int H = Cfg::H, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP;
-    static constexpr int DPX = Cfg::DPX;
+    static constexpr int H = Cfg::H, HX = Cfg::HX, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS;
+    static constexpr int NP = Cfg::NP, DPX = Cfg::DPX;
 
     const StageArgs<T> &A;
     unsigned char *sm;
     int x0, y0;
 
-    __device__ __forceinline__ C *yslot(int s) const { return reinterpret_cast<C *>(sm + s * Cfg::YSLOT) + H * PX + H; }
+    __device__ __forceinline__ C *yslot(int s) const { return reinterpret_cast<C *>(sm + s * Cfg::YSLOT) + H * PX + HX; }
     __device__ __forceinline__ C *dslot(int s) const {
         return reinterpret_cast<C *>(sm + Cfg::OFF_D + s * Cfg::DSLOT) + DPX + 1;
     }
@@ -124,6 +132,7 @@ struct T3Body {
     // Boundary D at a face point b (Laplacian form of the BC, (BCDlap) P:320-323 /
     // (BCMSDlap) P:336-344), given Y_b, and Y, D at the inward normal neighbour b'.
     __device__ __forceinline__ C D_bc(int64_t qb, C yb, int64_t qb1, C y1, C d1) const {
+        if (BC == BC_L0) { C z; z.x = T(0); z.y = T(0); return z; }   // (BCL0lap) P:352-355
         const T nb = nlin(qb, yb);
         if (BC == BC_DIRICHLET) {
             const T t = A.c.inv_a * nb;
@@ -190,7 +199,7 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, int64_t q, int 
     } else if (STAGE == 4) {
         const C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
         store_out(A, q, z, r4);
-        if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, A.step);
+        if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
         A.K[q] = cadd(kt, cscale(T(2), F));
         store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
@@ -224,7 +233,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             return;
         }
         mbar_expect_tx(bar, Cfg::YBYTES);
-        tma_load_3d(smem_u32(sm + s * Cfg::YSLOT), mY, 2 * (x0 - H), y0 - H, p + g.zghost, bar);
+        tma_load_3d(smem_u32(sm + s * Cfg::YSLOT), mY, 2 * (x0 - Cfg::HX), y0 - H, p + g.zghost, bar);
     };
     auto issue_pkv = [&](int p) {
         if (p >= ze || pkv_bytes == 0) return;
@@ -238,15 +247,20 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         }
         if (A.V) tma_load_3d(smem_u32(dst + 2 * Cfg::OWN_C), mV, x0, y0, p, bar);
     };
+    // the TMA issuer: lane 0 of the last warp (no ring work there)
+    const bool issuer = (tid == Cfg::NT - 32);
+    const unsigned cbar0 = bar0 + 8 * (NS + NP);      // two CTA barriers (2SHOC)
 
     if (tid == 0) {
         for (int i = 0; i < NS + NP; i++) mbar_init(bar0 + 8 * i, 1);
+        mbar_init(cbar0, Cfg::NT);
+        mbar_init(cbar0 + 8, Cfg::NT);
         fence_proxy_async();
     }
     __syncthreads();
-    if (tid == 0) {
+    if (issuer) {
         for (int p = zbase; p <= zs + H + P - 1; p++) issue_y(p);
-        for (int p = zs; p <= zs + P - 1; p++) issue_pkv(p);
+        for (int p = zs; p <= zs + Cfg::PP - 1; p++) issue_pkv(p);
     }
 
     const int gx = x0 + tx, gy = y0 + ty;
@@ -288,7 +302,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         mbar_wait(bar0 + 8 * s0, 0);
         C ym = b.yslot(sm1)[own], yc = b.yslot(s0)[own];
         for (int z = zs; z < ze; z++) {
-            if (tid == 0) { issue_y(z + H + P); issue_pkv(z + P); }
+            if (issuer) { issue_y(z + H + P); issue_pkv(z + Cfg::PP); }
             mbar_wait(bar0 + 8 * s1, par1);
             const C *Y0 = b.yslot(s0) + own;
             const C yp = b.yslot(s1)[own];
@@ -313,26 +327,37 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     }
 
     // ---------------------------------------------------------------- 2SHOC
-    // Y slots of planes z-1, z, z+1, z+2 at z = zs: relative indices 1, 2, 3, 4
-    int sm1 = 1, s0 = 2, s1 = 3, s2 = 4;
+    // Barrier protocol (no __syncthreads in the loop): phase j = "every thread has written
+    // D(zs + j) to shared memory"; it completes on CTA barrier cbar[j & 1] (arrival count
+    // NT) as that barrier's (j >> 1)-th phase, so a waiter can never see its barrier two
+    // phases ahead.  In iteration z = zs + j a thread writes D(z+1), arrives on phase j+1,
+    // then waits for phase j before reading D(z) of its neighbours.  Having passed phase
+    // j-1 (in iteration z-1) implies every thread finished iteration z-3: the TMA refills
+    // at the top of iteration z therefore target the slots of plane z-3, and D(z+1) goes
+    // into the slot of D(z-3) (4 D slots).
+    // Register queues: yq = Y centre at (z, z+1, z+2), dq = D at (z-1, z, z+1), pxq / pyq =
+    // pair sums at (z-1, z, z+1), stored with period 3; the z loop is unrolled by 3 so the
+    // queue rotation is pure register renaming.
+    int sm1 = 1, s0 = 2, s1 = 3, s2 = 4;              // Y slots of planes z-1 .. z+2 at z = zs
     unsigned par2 = 0;                                // parity of plane z+2's slot use
     if (zs - 2 >= zl_lo) mbar_wait(bar0 + 0, 0);
     mbar_wait(bar0 + 8 * sm1, 0);
     mbar_wait(bar0 + 8 * s0, 0);
     mbar_wait(bar0 + 8 * s1, 0);
-    int d0s = 0;                                      // D slot of plane z (3-plane ring)
-    C yz = b.yslot(s0)[own], yz1 = b.yslot(s1)[own];
-    C px0, py0, pxm, pym, d0, dm;
+    int d0s = 0;                                      // D slot of plane z (4-plane ring)
+    C yq[3], dq[3], pxq[3], pyq[3];
+    yq[0] = b.yslot(s0)[own];
+    yq[1] = b.yslot(s1)[own];
     {
         const C *Y0 = b.yslot(s0) + own, *Ym = b.yslot(sm1) + own;
-        px0 = cadd(Y0[-1], Y0[1]);
-        py0 = cadd(Y0[-PX], Y0[PX]);
-        pxm = cadd(Ym[-1], Ym[1]);
-        pym = cadd(Ym[-PX], Ym[PX]);
+        pxq[1] = cadd(Y0[-1], Y0[1]);
+        pyq[1] = cadd(Y0[-PX], Y0[PX]);
+        pxq[0] = cadd(Ym[-1], Ym[1]);
+        pyq[0] = cadd(Ym[-PX], Ym[PX]);
         // D(zs) at the owned point and the ring (zs is never a z face)
-        if (EDGE) d0 = b.D_gen(zs, sm1, s0, s1, 0, tx, ty);
-        else d0 = b.D_int(Ym, Y0, b.yslot(s1) + own);
-        b.dslot(d0s)[downo] = d0;
+        if (EDGE) dq[1] = b.D_gen(zs, sm1, s0, s1, 0, tx, ty);
+        else dq[1] = b.D_int(Ym, Y0, b.yslot(s1) + own);
+        b.dslot(d0s)[downo] = dq[1];
         if (ring) {
             C dr;
             if (EDGE) dr = b.D_gen(zs, sm1, s0, s1, 0, rlx, rly);
@@ -341,41 +366,44 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         }
         // D(zs - 1) at the owned point (used only there): BC form on the lower z face,
         // else the stencil
-        dm = d0;
+        dq[0] = dq[1];
         if (!out_ok) {
         } else if (g.zf_lo && zs - 1 == 0) {
-            dm = b.D_bc(int64_t(qrow), Ym[0], int64_t(g.sz) + qrow, yz, d0);
+            dq[0] = b.D_bc(int64_t(qrow), Ym[0], int64_t(g.sz) + qrow, yq[0], dq[1]);
         } else {
             const C *Ymm = b.yslot(0) + own;
             const C y2 = cadd(Ym[0], Ym[0]);
-            C acc = csub(pxm, y2);
-            acc = cadd(acc, csub(pym, y2));
-            acc = cadd(acc, csub(cadd(Ymm[0], yz), y2));
-            dm = cscale(A.c.ih2, acc);
+            C acc = csub(pxq[0], y2);
+            acc = cadd(acc, csub(pyq[0], y2));
+            acc = cadd(acc, csub(cadd(Ymm[0], yq[0]), y2));
+            dq[0] = cscale(A.c.ih2, acc);
         }
     }
-    __syncthreads();
+    mbar_arrive(cbar0);                               // phase 0: D(zs) written
+    int j = 0;                                        // z - zs
 
-    for (int z = zs; z < ze; z++) {
-        if (tid == 0) { issue_y(z + H + P); issue_pkv(z + P); }
+    auto body = [&](auto phase, int z) {
+        constexpr int PH = decltype(phase)::value;
+        constexpr int I0 = PH, I1 = (PH + 1) % 3, I2 = (PH + 2) % 3;
+        if (issuer) { issue_y(z + H + P); issue_pkv(z + Cfg::PP); }
         const bool zf1 = g.zf_hi && (z + 1 == nz - 1);       // D(z+1) by the BC form
-        const int d1s = (d0s == 2) ? 0 : d0s + 1;
+        const int d1s = (d0s + 1) & 3;
         if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
         const C *Y0 = b.yslot(s0) + own, *Y1 = b.yslot(s1) + own;
         const C px1 = cadd(Y1[-1], Y1[1]);
         const C py1 = cadd(Y1[-PX], Y1[PX]);
-        C yz2 = yz1, dn;
+        C yz2 = yq[I1], dn;
         if (EDGE) {
             dn = b.D_gen(z + 1, s0, s1, s2, d0s, tx, ty);
             if (!zf1) yz2 = b.yslot(s2)[own];
         } else if (zf1) {
-            dn = b.D_bc(int64_t(z + 1) * g.sz + qrow, yz1, int64_t(z) * g.sz + qrow, yz, d0);
+            dn = b.D_bc(int64_t(z + 1) * g.sz + qrow, yq[I1], int64_t(z) * g.sz + qrow, yq[I0], dq[I1]);
         } else {
             yz2 = b.yslot(s2)[own];
-            const C y2 = cadd(yz1, yz1);
+            const C y2 = cadd(yq[I1], yq[I1]);
             C acc = csub(px1, y2);
             acc = cadd(acc, csub(py1, y2));
-            acc = cadd(acc, csub(cadd(yz, yz2), y2));
+            acc = cadd(acc, csub(cadd(yq[I0], yz2), y2));
             dn = cscale(A.c.ih2, acc);
         }
         b.dslot(d1s)[downo] = dn;
@@ -391,36 +419,43 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             }
             b.dslot(d1s)[rdo] = dr;
         }
-        __syncthreads();
-
+        mbar_arrive(cbar0 + 8 * ((j + 1) & 1));            // phase j+1: D(z+1) written
         C psi, kt; T v;
         pkv_wait();
         load_own(psi, kt, v);
+        // 2SHOC step 2, grouping of DESIGN.md §3.1: the parts that need no
+        // neighbour D first, then wait for phase j (D(z) of the whole tile + ring)
+        const C y4 = cscale(T(4), yq[I0]);
+        const C pxa = cadd(Y0[-PX - 1], Y0[-PX + 1]);
+        const C pxb = cadd(Y0[PX - 1], Y0[PX + 1]);
+        const C exy = csub(cadd(pxa, pxb), y4);
+        const C exz = csub(cadd(pxq[I0], px1), y4);
+        const C eyz = csub(cadd(pyq[I0], py1), y4);
+        const C E = cadd(cadd(exy, exz), eyz);
+        mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
         if (out_ok) {
-            // 2SHOC step 2, grouping of DESIGN.md §3.1
-            const C y4 = cscale(T(4), yz);
-            const C pxa = cadd(Y0[-PX - 1], Y0[-PX + 1]);
-            const C pxb = cadd(Y0[PX - 1], Y0[PX + 1]);
-            const C exy = csub(cadd(pxa, pxb), y4);
-            const C exz = csub(cadd(pxm, px1), y4);
-            const C eyz = csub(cadd(pym, py1), y4);
-            const C E = cadd(cadd(exy, exz), eyz);
             const C *Dz = b.dslot(d0s) + downo;
-            const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dm, dn));
-            const C td = csub(sd, cscale(T(10), d0));
+            const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dq[I0], dn));
+            const C td = csub(sd, cscale(T(10), dq[I1]));
             const C L = csub(cscale(A.c.c16h2, E), cscale(A.c.c112, td));
-            t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yz, L, psi, kt, v);
+            t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yq[I0], L, psi, kt, v);
         }
-        // rotate the register queues and the rings
-        dm = d0; d0 = dn;
-        pxm = px0; px0 = px1;
-        pym = py0; py0 = py1;
-        yz = yz1; yz1 = yz2;
+        // queue update (the slots of plane z-1 become those of plane z+2) and ring rotation
+        dq[I2] = dn; pxq[I2] = px1; pyq[I2] = py1; yq[I2] = yz2;
         sm1 = s0; s0 = s1; s1 = s2;
         if (++s2 == NS) { s2 = 0; par2 ^= 1u; }
         d0s = d1s;
         pkv_next();
+        ++j;
+    };
+    int z = zs;
+    for (; z + 3 <= ze; z += 3) {
+        body(std::integral_constant<int, 0>(), z);
+        body(std::integral_constant<int, 1>(), z + 1);
+        body(std::integral_constant<int, 2>(), z + 2);
     }
+    if (z < ze) body(std::integral_constant<int, 0>(), z++);
+    if (z < ze) body(std::integral_constant<int, 1>(), z++);
 }
 
 template <typename T, int ORDER, int BC, int STAGE, int P>

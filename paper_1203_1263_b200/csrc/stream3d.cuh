@@ -118,6 +118,7 @@ struct S3 {
     // Boundary D on a face point b (Laplacian-form BC, (BCDlap) P:320-323 / (BCMSDlap)
     // P:336-344), given Y_b, Y_b' and D_b' (b' = inward normal neighbour).
     __device__ __forceinline__ C D_face_val(int64_t qb, C yb, int64_t qb1, C y1, C d1) const {
+        if (BC == BC_L0) { C z; z.x = T(0); z.y = T(0); return z; }   // (BCL0lap) P:352-355
         const T nb = nlin(qb, yb);
         if (BC == BC_DIRICHLET) {
             T t = A.c.inv_a * nb;
@@ -176,7 +177,7 @@ __device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, i
     } else if (STAGE == 4) {
         C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
         store_out(A, q, z, r4);
-        if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, A.step);
+        if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
         A.K[q] = cadd(kt, cscale(T(2), F));
         store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
@@ -184,7 +185,7 @@ __device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, i
 }
 
 template <typename T, int ORDER, int BC, int STAGE, int RY>
-__global__ void __launch_bounds__(S3_THREADS, (sizeof(T) == 8 ? (RY == 1 ? 3 : 2) : 3))
+__global__ void __launch_bounds__(S3_THREADS, (sizeof(T) == 8 ? 2 : 3))
 stage3d_stream(StageArgs<T> A, int zchunk) {
     using C = cplx<T>;
     using Cfg = S3Cfg<T, ORDER, RY>;

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
                 const bool fx = (gx == 0 || gx == nx - 1), fy = (gy == 0 || gy == ny - 1);
                 if (!fx && !fy) {
                     d = D_int(lx, ly);
+                } else if (BC == BC_L0 && !(fx && fy)) {
+                    d.x = T(0); d.y = T(0);                       // (BCL0lap) P:352-355
                 } else if (!(fx && fy)) {
                     // face: Laplacian form of the BC with b' the in-plane inward neighbour
                     const C yb = Ys(lx, ly);

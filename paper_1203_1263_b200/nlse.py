@@ -15,13 +15,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libnlse_b200.so")
 
 NLSE_OK, NLSE_ERR_ARG, NLSE_ERR_UNSTABLE, NLSE_ERR_OOM, NLSE_ERR_CUDA, NLSE_ERR_COMM, NLSE_ERR_DIVERGED = range(7)
-NLSE_BC_DIRICHLET, NLSE_BC_MSD = 0, 1
+NLSE_BC_DIRICHLET, NLSE_BC_MSD, NLSE_BC_L0 = 0, 1, 2
 NLSE_CD2, NLSE_2SHOC4 = 2, 4
 NLSE_FP32, NLSE_FP64 = 4, 8
 NLSE_FLAG_FORCE_DT, NLSE_FLAG_GENERIC_KERNELS = 1, 2
 NLSE_MAX_KINDS = 8
 
-BC = {"dirichlet": NLSE_BC_DIRICHLET, "msd": NLSE_BC_MSD}
+BC = {"dirichlet": NLSE_BC_DIRICHLET, "msd": NLSE_BC_MSD, "l0": NLSE_BC_L0}
 ORDER = {"cd": NLSE_CD2, "2shoc": NLSE_2SHOC4}
 PREC = {"fp32": NLSE_FP32, "fp64": NLSE_FP64}
 
@@ -139,7 +139,7 @@ class Solver:
                  force_dt=False, generic=False, dist=None):
         self.dims = tuple(int(d) for d in dims)
         self.dist = dist
-        if dist is not None:
+        if dist is not None and len(self.dims) == 3:
             rank, nranks = dist
             self.z0, nloc = nlse_slab_range(self.dims[2], nranks, rank)
             self.shape = (nloc,) + tuple(reversed(self.dims[:2]))

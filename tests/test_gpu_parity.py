@@ -25,7 +25,7 @@ def _k(ndim, h, scheme):
 @pytest.mark.parametrize("kernel", ["fast", "v1", "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 @pytest.mark.parametrize("ndim", [1, 2, 3])
 def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch):
@@ -54,7 +54,7 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
 
 @pytest.mark.parametrize("dims", [(3,), (4,), (3, 3), (3, 5), (5, 3), (3, 3, 3), (4, 3, 5), (3, 7, 3), (9, 3, 4)])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
-@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 def test_degenerate_small_grids(dims, scheme, bc):
     """The smallest legal grids (3 points per axis: one interior layer) and thin slabs."""
     psi0 = case_input(dims, seed=5)
@@ -197,3 +197,34 @@ def test_device_io_roundtrip():
             torch.cuda.synchronize()
             assert torch.equal(t, u)
             assert np.array_equal(sv.nlse_get_psi(), t.cpu().numpy().astype(np.complex128))
+
+
+def test_cuda_graph_replay_matches_direct_launches(monkeypatch):
+    """nlse_step with many steps replays a captured CUDA graph of 8 steps (device-side step
+    counter and barrier epochs); the result and the divergence step index equal the
+    direct-launch path bit for bit."""
+    dims = (40, 21, 19)
+    psi0 = case_input(dims, seed=61)
+    k = _k(3, 0.5, "2shoc")
+    a = run_gpu(dims, 0.5, psi0, k, 37, s=-1.0, bc="msd")                     # 4 graph replays + 5
+    monkeypatch.setenv("NLSE_GRAPHS", "0")
+    b = run_gpu(dims, 0.5, psi0, k, 37, s=-1.0, bc="msd", chunks=[5, 32])
+    assert ulp_diff(a, b, "fp64") == 0
+    ref = run_oracle(dims, 0.5, psi0, k, 37, s=-1.0, bc="msd")
+    assert ulp_diff(a, ref, "fp64") == 0
+
+
+def test_divergence_step_index_with_graphs():
+    from paper_1203_1263_b200.nlse import NLSE_ERR_DIVERGED, NLSEError, Solver
+    dims = (31, 17)
+    psi = case_input(dims, seed=3)
+    msgs = []
+    for chunks in ([400], [3, 397]):
+        with Solver(dims, 0.1, s=-1.0, bc="dirichlet", force_dt=True) as sv:
+            sv.nlse_set_psi(psi)
+            with pytest.raises(NLSEError) as e:
+                for n in chunks:
+                    sv.nlse_step(0.05, n)
+            assert e.value.status == NLSE_ERR_DIVERGED
+            msgs.append(str(e.value))
+    assert msgs[0] == msgs[1], msgs

@@ -21,7 +21,7 @@ def _k(h, scheme):
 
 @pytest.mark.parametrize("nranks", [2, 3, 5])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-@pytest.mark.parametrize("bc", ["dirichlet", "msd"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 def test_slabs_bitwise_equal_single(scheme, bc, precision, nranks):
     dims = (70, 37, 29)
