@@ -38,7 +38,7 @@ static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
 
 struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
 
-constexpr int TMA_P = 2;        // TMA ring prefetch depth (planes ahead)
+constexpr int TMA_P = 3;        // TMA ring prefetch depth of the Y planes (planes ahead)
 constexpr int GRAPH_STEPS = 8;  // RK4 steps per captured CUDA graph
 
 enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2 };
@@ -98,6 +98,7 @@ struct nlse_ctx {
     int64_t kind_points[KK_COUNT] = {0};
     int interior_kind = KK_GENERIC;
     bool tma = false;
+    int tma_ty = 8;                  // TMA kernel tile height (8: 256 threads, 16: 512 threads)
     Tma3Maps maps{};
     // slab mode
     bool dist = false;
@@ -213,9 +214,9 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
     return r == CUDA_SUCCESS;
 }
 
-template <typename T, int ORDER>
+template <typename T, int ORDER, int TYV>
 bool build_maps(nlse_ctx *c) {
-    using Cfg = T3Cfg<T, ORDER, TMA_P>;
+    using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
     const uint64_t nx = c->g.nx, ny = c->g.ny, nz = c->g.nz, nza = nz + 2 * c->g.zghost;
     const int eb = int(sizeof(T));
     bool ok = true;
@@ -233,29 +234,51 @@ bool build_maps(nlse_ctx *c) {
 int ybuf_of_stage(int stage) { return stage == 1 ? BUF_PSI : (stage == 3 ? BUF_OUT : BUF_TMP); }
 int obuf_of_stage(int stage) { return stage == 1 ? BUF_TMP : (stage == 2 ? BUF_OUT : (stage == 3 ? BUF_TMP : BUF_PSI)); }
 
-template <typename T, int ORDER, int BC, int STAGE>
-void launch_tma3d(nlse_ctx *c, const StageArgs<T> &A) {
-    using Cfg = T3Cfg<T, ORDER, TMA_P>;
+template <typename T, int ORDER, int BC, int STAGE, int TYV>
+void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
+    using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
     const int64_t nx = A.g.nx, ny = A.g.ny;
     const int64_t mz = A.g.nz - A.g.zf_lo - A.g.zf_hi;
     const unsigned gx = unsigned((nx + Cfg::TX - 1) / Cfg::TX);
     const unsigned gy = unsigned((ny + Cfg::TY - 1) / Cfg::TY);
-    // z chunks: about two waves of resident CTAs, chunks of at least 8 planes
+    // z chunks of 128 planes (L2 locality of the persistent walk, see stage3d_tma), fewer
+    // for small grids so that there are about two items per resident CTA
     const int64_t cols = int64_t(gx) * gy;
-    const int64_t resident = 148 * (sizeof(T) == 8 ? 2 : 3);
+    const int64_t resident = 148 * (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2));
     const int64_t want = (2 * resident + cols - 1) / cols;
-    int64_t zchunk = (mz + want - 1) / want;
+    int64_t zchunk = std::min<int64_t>(128, (mz + want - 1) / want);
     if (zchunk < 8) zchunk = 8;
+    static const int64_t env_chunk = [] {
+        const char *e = getenv("NLSE_ZCHUNK");
+        return e ? std::atoll(e) : int64_t(0);
+    }();
+    if (env_chunk > 0) zchunk = env_chunk;
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg::SMEM);
-        attr_set = true;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+                                                      Cfg::NT, Cfg::SMEM);
+        if (per_sm < 1) per_sm = 1;
     }
-    stage3d_tma<T, ORDER, BC, STAGE, TMA_P><<<dim3(gx, gy, gz), Cfg::NT, Cfg::SMEM, c->stream>>>(
-        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk));
+    static int nsm = 0;
+    if (!nsm) {
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+        if (nsm < 1) nsm = 148;
+    }
+    const int64_t items = int64_t(gx) * gy * gz;
+    const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(nsm) * per_sm));
+    stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<grid, Cfg::NT, Cfg::SMEM, c->stream>>>(
+        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
+        int(gz));
+}
+
+template <typename T, int ORDER, int BC, int STAGE>
+void launch_tma3d(nlse_ctx *c, const StageArgs<T> &A) {
+    if (c->tma_ty == 16) launch_tma3d_ty<T, ORDER, BC, STAGE, 16>(c, A);
+    else launch_tma3d_ty<T, ORDER, BC, STAGE, 8>(c, A);
 }
 
 // One stage: interior kernel family + boundary kernel (or the generic kernel over the
@@ -690,9 +713,16 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     if (c->interior_kind == KK_TMA3D) {
         const std::string ek = env_kernel();
         bool ok = ek != "v1";
+        const char *ety = getenv("NLSE_TMA_TY");
+        c->tma_ty = (ety && std::atoi(ety) == 16) ? 16 : 8;
         if (ok) {
-            if (prec == NLSE_FP64) ok = order == NLSE_2SHOC4 ? build_maps<double, ORDER_2SHOC>(c) : build_maps<double, ORDER_CD>(c);
-            else ok = order == NLSE_2SHOC4 ? build_maps<float, ORDER_2SHOC>(c) : build_maps<float, ORDER_CD>(c);
+            auto bm = [&](auto TYc) {
+                constexpr int TYV = decltype(TYc)::value;
+                if (prec == NLSE_FP64)
+                    return order == NLSE_2SHOC4 ? build_maps<double, ORDER_2SHOC, TYV>(c) : build_maps<double, ORDER_CD, TYV>(c);
+                return order == NLSE_2SHOC4 ? build_maps<float, ORDER_2SHOC, TYV>(c) : build_maps<float, ORDER_CD, TYV>(c);
+            };
+            ok = c->tma_ty == 16 ? bm(std::integral_constant<int, 16>()) : bm(std::integral_constant<int, 8>());
         }
         // TMA needs 16-byte row strides (complex rows: nx even for fp32; V rows: nx*sizeof(T) % 16)
         if (!ok) c->interior_kind = KK_STREAM3D;

@@ -55,6 +55,9 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_inval(unsigned bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap *map, int c0, int c1, int c2,
                                             unsigned bar) {
@@ -65,20 +68,20 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap *map
 }
 
 // ------------------------------------------------------------------ configuration
-template <typename T, int ORDER, int P>
+template <typename T, int ORDER, int P, int TYV = 8>
 struct T3Cfg {
     static constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
     // x halo of the staged tile: a TMA box must start on a 16-byte boundary, so fp32 tiles
     // carry a 2-point x halo even for CD (x0 is a multiple of 32)
     static constexpr int HX = (sizeof(T) == 4) ? 2 : H;
-    static constexpr int TX = 32, TY = 8, NT = TX * TY;
+    static constexpr int TX = 32, TY = TYV, NT = TX * TY;   // lane = x, warp = y
     static constexpr int PX = TX + 2 * HX, PY = TY + 2 * H;
     static constexpr int CB = 2 * int(sizeof(T));                   // bytes per complex value
-    // Psi/K/V prefetch depth (planes ahead); Y uses P.  A slot is refilled only after every
-    // thread has finished the plane three planes back (see the barrier protocol in t3_run),
-    // hence ring sizes P + 5 (Y: planes z..z+2 in use) and PP + 3.
-    static constexpr int PP = (sizeof(T) == 8) ? 1 : 2;
-    static constexpr int NS = P + 5, NP = PP + 3, ND = (ORDER == ORDER_2SHOC) ? 4 : 0;
+    // Psi/K/V prefetch depth (planes ahead); Y uses P.  A slot is refilled only once every
+    // thread has finished the plane two planes back (see the barrier protocol in t3_run),
+    // hence ring sizes P + 4 (Y: the planes in use reach two ahead) and PP + 2.
+    static constexpr int PP = (sizeof(T) == 8) ? 2 : 3;
+    static constexpr int NS = P + 4, NP = PP + 2, ND = (ORDER == ORDER_2SHOC) ? 4 : 0;
     static constexpr int DPX = TX + 2, DPY = TY + 2;
     static constexpr int up128(int b) { return (b + 127) / 128 * 128; }
     static constexpr int YBYTES = PX * PY * CB;
@@ -103,10 +106,10 @@ struct Tma3Maps {
     CUtensorMap psi, k, v;
 };
 
-template <typename T, int ORDER, int BC, int STAGE, int P, bool EDGE>
+template <typename T, int ORDER, int BC, int STAGE, int P, int TYV, bool EDGE>
 struct T3Body {
     using C = cplx<T>;
-    using Cfg = T3Cfg<T, ORDER, P>;
+    using Cfg = T3Cfg<T, ORDER, P, TYV>;
     static constexpr int H = Cfg::H, HX = Cfg::HX, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS;
     static constexpr int NP = Cfg::NP, DPX = Cfg::DPX;
 
@@ -206,13 +209,13 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, int64_t q, int 
     }
 }
 
-template <typename T, int ORDER, int BC, int STAGE, int P, bool EDGE>
+template <typename T, int ORDER, int BC, int STAGE, int P, int TYV, bool EDGE>
 __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap *mP, const CUtensorMap *mK,
                                        const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
                                        int y0, int zs, int ze) {
     using C = cplx<T>;
-    using Cfg = T3Cfg<T, ORDER, P>;
-    using B = T3Body<T, ORDER, BC, STAGE, P, EDGE>;
+    using Cfg = T3Cfg<T, ORDER, P, TYV>;
+    using B = T3Body<T, ORDER, BC, STAGE, P, TYV, EDGE>;
     constexpr int H = Cfg::H, TX = Cfg::TX, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
     const B b{A, sm, x0, y0};
     const Grid &g = A.g;
@@ -331,10 +334,10 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     // D(zs + j) to shared memory"; it completes on CTA barrier cbar[j & 1] (arrival count
     // NT) as that barrier's (j >> 1)-th phase, so a waiter can never see its barrier two
     // phases ahead.  In iteration z = zs + j a thread writes D(z+1), arrives on phase j+1,
-    // then waits for phase j before reading D(z) of its neighbours.  Having passed phase
-    // j-1 (in iteration z-1) implies every thread finished iteration z-3: the TMA refills
-    // at the top of iteration z therefore target the slots of plane z-3, and D(z+1) goes
-    // into the slot of D(z-3) (4 D slots).
+    // then waits for phase j before reading D(z) of its neighbours.  Passing phase j means
+    // every thread has finished iteration z-2, so right after that wait the issuer refills
+    // the Y and Psi/K/V slots of plane z-2; D(z+1) (written before the wait, when only
+    // phase j-1 is known) goes into the slot of D(z-3) (4 D slots).
     // Register queues: yq = Y centre at (z, z+1, z+2), dq = D at (z-1, z, z+1), pxq / pyq =
     // pair sums at (z-1, z, z+1), stored with period 3; the z loop is unrolled by 3 so the
     // queue rotation is pure register renaming.
@@ -385,7 +388,6 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     auto body = [&](auto phase, int z) {
         constexpr int PH = decltype(phase)::value;
         constexpr int I0 = PH, I1 = (PH + 1) % 3, I2 = (PH + 2) % 3;
-        if (issuer) { issue_y(z + H + P); issue_pkv(z + Cfg::PP); }
         const bool zf1 = g.zf_hi && (z + 1 == nz - 1);       // D(z+1) by the BC form
         const int d1s = (d0s + 1) & 3;
         if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
@@ -420,9 +422,6 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             b.dslot(d1s)[rdo] = dr;
         }
         mbar_arrive(cbar0 + 8 * ((j + 1) & 1));            // phase j+1: D(z+1) written
-        C psi, kt; T v;
-        pkv_wait();
-        load_own(psi, kt, v);
         // 2SHOC step 2, grouping of DESIGN.md §3.1: the parts that need no
         // neighbour D first, then wait for phase j (D(z) of the whole tile + ring)
         const C y4 = cscale(T(4), yq[I0]);
@@ -433,6 +432,10 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         const C eyz = csub(cadd(pyq[I0], py1), y4);
         const C E = cadd(cadd(exy, exz), eyz);
         mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
+        if (issuer) { issue_y(z + H + P); issue_pkv(z + Cfg::PP); }
+        C psi, kt; T v;
+        pkv_wait();
+        load_own(psi, kt, v);
         if (out_ok) {
             const C *Dz = b.dslot(d0s) + downo;
             const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dq[I0], dn));
@@ -458,24 +461,43 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     if (z < ze) body(std::integral_constant<int, 1>(), z++);
 }
 
-template <typename T, int ORDER, int BC, int STAGE, int P>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 ? 2 : 3))
+// Persistent launch: gridDim.x CTAs (the resident count) walk the work items
+// w = blockIdx.x, blockIdx.x + gridDim.x, ... ordered z-chunk-major, then tile row, then
+// tile column.  All resident CTAs start together on consecutive tiles of one z chunk and
+// advance through z at the same rate, so the halo rows and columns a tile shares with its
+// neighbours are still in L2 when the neighbour loads them (with one CTA per tile in a
+// plain grid, CTAs start whenever a slot frees and drift apart by far more planes than
+// the ~25 us L2 residency at full HBM rate).
+template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
+__global__ void __launch_bounds__(32 * TYV, (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2)))
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
-            const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV, StageArgs<T> A,
-            int zchunk) {
-    using Cfg = T3Cfg<T, ORDER, P>;
+            const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
+            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int nchunks) {
+    using Cfg = T3Cfg<T, ORDER, P, TYV>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int x0 = blockIdx.x * Cfg::TX, y0 = blockIdx.y * Cfg::TY;
     const int nz = int(A.g.nz);
     const int zlo = A.g.zf_lo ? 1 : 0, zhi = nz - (A.g.zf_hi ? 1 : 0);
-    const int zs = zlo + blockIdx.z * zchunk;
-    const int ze = min(zs + zchunk, zhi);
-    if (zs >= ze) return;
     const int nx = int(A.g.nx), ny = int(A.g.ny);
-    // every owned and ring point in-plane interior -> branch-free path
-    const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
-    if (edge) t3_run<T, ORDER, BC, STAGE, P, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
-    else t3_run<T, ORDER, BC, STAGE, P, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    const int ntiles = ntx * nty;
+    const int total = ntiles * nchunks;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        const int c = w / ntiles, t = w - c * ntiles;
+        const int x0 = (t % ntx) * Cfg::TX, y0 = (t / ntx) * Cfg::TY;
+        const int zs = zlo + c * zchunk;
+        const int ze = min(zs + zchunk, zhi);
+        if (zs < ze) {
+            // every owned and ring point in-plane interior -> branch-free path
+            const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
+            if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+            else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+        }
+        // retire this item's barriers before the next item re-initialises them
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned bar0 = smem_u32(smem_raw + Cfg::OFF_BAR);
+            for (int i = 0; i < Cfg::NS + Cfg::NP + 2; i++) mbar_inval(bar0 + 8 * i);
+        }
+    }
 }
 
 }  // namespace nlse
