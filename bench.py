@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--generic", action="store_true", help="use the one-thread-per-point kernels")
+    ap.add_argument("--scheme", default=None, help="override the workload's scheme (cd | 2shoc), for experiments")
+    ap.add_argument("--precision", default=None, help="override the workload's precision (fp32 | fp64)")
     return ap.parse_args()
 
 
@@ -249,6 +251,10 @@ def main():
     from paper_1203_1263_b200.nlse import Solver
 
     cfg = workload(args.config, rank, world)
+    if args.scheme:
+        cfg["scheme"] = args.scheme
+    if args.precision:
+        cfg["precision"] = args.precision
     B = bytes_min_per_point(cfg)
     peak, peak_src = measured_peaks()
     npts = int(np.prod(cfg["dims"]))              # whole job

@@ -194,7 +194,8 @@ nlse_status nlse_reset_timing(nlse_ctx *ctx);
 
 typedef struct {
     int64_t points;            /* prod(dims) */
-    int64_t launches_per_step; /* kernel launches per RK4 step */
+    int64_t launches_per_step; /* kernel launches per RK4 step (0: 1D grids run all steps of an
+                                  nlse_step call in one persistent launch) */
     int64_t min_bytes_per_step;/* algorithmic HBM bytes per RK4 step, (16c + 4 r_V) * points */
     int64_t device_bytes;      /* device memory held by the context */
     int elem_bytes;            /* sizeof(real): 4 or 8 */

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "diag.cuh"
 #include "generic.cuh"
+#include "persist1d.cuh"
 #include "stage3d_tma.cuh"
 #include "stream3d.cuh"
 #include "tile2d.cuh"
@@ -85,6 +86,8 @@ struct nlse_ctx {
     int diag_blocks = 0;
     cudaStream_t stream = nullptr;
     std::shared_ptr<StreamHolder> stream_ref;   // virtual ranks of one group share one stream
+    cudaStream_t side_stream = nullptr;          // 3D boundary kernel, forked / joined per stage
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int device = 0;
     int64_t steps_done = 0;
     int64_t device_bytes = 0;
@@ -112,6 +115,7 @@ struct nlse_ctx {
     std::vector<void *> ipc_opened;
     bool ghost_stale = false;
     bool virtual_group = false;      // connected by nlse_dist_connect_local: _group calls only
+    bool persist1d = false;          // 1D: one persistent CTA per nlse_step call
 };
 
 namespace {
@@ -255,24 +259,15 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     if (env_chunk > 0) zchunk = env_chunk;
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
-    static int per_sm = 0;
-    if (!per_sm) {
+    static bool attr_set = false;
+    if (!attr_set) {
         cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
-                                                      Cfg::NT, Cfg::SMEM);
-        if (per_sm < 1) per_sm = 1;
-    }
-    static int nsm = 0;
-    if (!nsm) {
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-        if (nsm < 1) nsm = 148;
+        attr_set = true;
     }
     const int64_t items = int64_t(gx) * gy * gz;
-    const unsigned grid = unsigned(std::min<int64_t>(items, int64_t(nsm) * per_sm));
-    stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<grid, Cfg::NT, Cfg::SMEM, c->stream>>>(
-        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
-        int(gz));
+    stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
+        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy));
 }
 
 template <typename T, int ORDER, int BC, int STAGE>
@@ -290,6 +285,17 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
         stage_generic<T, DIM, ORDER, BC, STAGE><<<blocks_for(c->g.n, 256), 256, 0, c->stream>>>(A);
         return;
     }
+    // 3D: the boundary kernel (disjoint outputs, same inputs) runs concurrently on a side
+    // stream, forked from and joined back into the context stream (not in timing mode, so
+    // that per-kernel shares stay attributable)
+    const bool side = DIM == 3 && !c->timing && c->side_stream;
+    if (side) {
+        const int64_t nb = n_boundary_points<DIM>(c->g);
+        cudaEventRecord(c->ev_fork, c->stream);
+        cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0);
+        stage_boundary<T, DIM, ORDER, BC, STAGE><<<blocks_for(nb, 256), 256, 0, c->side_stream>>>(A);
+        cudaEventRecord(c->ev_join, c->side_stream);
+    }
     {
         const int64_t ni = (c->g.nx - 2) * (DIM >= 2 ? c->g.ny - 2 : 1) *
                            (DIM >= 3 ? c->g.nz - c->g.zf_lo - c->g.zf_hi : 1);
@@ -303,7 +309,9 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
             launch_tile1d<T, ORDER, BC, STAGE>(A, c->stream);
         }
     }
-    {
+    if (side) {
+        cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+    } else {
         const int64_t nb = n_boundary_points<DIM>(c->g);
         LaunchTimer lt(c, KK_BOUNDARY, nb);
         stage_boundary<T, DIM, ORDER, BC, STAGE><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
@@ -445,6 +453,39 @@ void enqueue_step_stage(nlse_ctx *c, int stage, double k, int64_t n, int mode = 
 
 void enqueue_add_steps(nlse_ctx *c, int64_t n) {
     add_steps<<<1, 1, 0, c->stream>>>(c->d_steps, int(n));
+}
+
+// 1D: all nsteps in one persistent CTA when the state fits in shared memory.
+template <typename T, int ORDER, int BC>
+void launch_persist1d(nlse_ctx *c, double k, int64_t nsteps) {
+    Persist1DArgs<T> P{};
+    P.psi = (cplx<T> *)c->buf[BUF_PSI];
+    P.V = (const T *)c->V;
+    P.n = int(c->g.nx);
+    P.c[0] = make_consts<T>(c, k / 2.0);
+    P.c[1] = make_consts<T>(c, k / 2.0);
+    P.c[2] = make_consts<T>(c, k);
+    P.c[3] = make_consts<T>(c, k / 6.0);
+    P.nsteps = nsteps;
+    P.diverged = c->d_div;
+    P.step_base = c->d_steps;
+    const size_t smem = persist1d_smem<T>(P.n, c->hasV, ORDER == ORDER_2SHOC);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(rk4_1d_persistent<T, ORDER, BC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        attr = true;
+    }
+    LaunchTimer lt(c, KK_TILE1D, c->g.n * nsteps);
+    rk4_1d_persistent<T, ORDER, BC><<<1, P1_THREADS, smem, c->stream>>>(P);
+}
+
+bool use_persist1d(const nlse_ctx *c) {
+    if (c->ndim != 1 || c->interior_kind == KK_GENERIC) return false;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const size_t need = c->prec == NLSE_FP64 ? persist1d_smem<double>(int(c->g.nx), c->hasV, c->order == NLSE_2SHOC4)
+                                             : persist1d_smem<float>(int(c->g.nx), c->hasV, c->order == NLSE_2SHOC4);
+    return c->g.nx <= (int64_t(1) << 30) && need <= size_t(optin);
 }
 
 void drop_graph(nlse_ctx *c) {
@@ -672,6 +713,11 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->stream_ref = std::make_shared<StreamHolder>();
     CREATE_TRY(cudaStreamCreateWithFlags(&c->stream_ref->s, cudaStreamNonBlocking));
     c->stream = c->stream_ref->s;
+    if (ndim == 3) {
+        CREATE_TRY(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+        CREATE_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CREATE_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
     const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.sz) * cb;
     const size_t halo_bytes = size_t(n) * cb + 2 * size_t(c->g.zghost) * plane;
     for (int b = 0; b < 3; b++) {
@@ -714,7 +760,7 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         const std::string ek = env_kernel();
         bool ok = ek != "v1";
         const char *ety = getenv("NLSE_TMA_TY");
-        c->tma_ty = (ety && std::atoi(ety) == 16) ? 16 : 8;
+        c->tma_ty = (ety && std::atoi(ety) == 8) ? 8 : 16;   // 16 measured faster (r01f, r01j)
         if (ok) {
             auto bm = [&](auto TYc) {
                 constexpr int TYV = decltype(TYc)::value;
@@ -729,6 +775,7 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         c->tma = ok;
     }
 #undef CREATE_TRY
+    c->persist1d = use_persist1d(c);
     c->connected = !dist;
     *out = c;
     return NLSE_OK;
@@ -787,6 +834,9 @@ void nlse_destroy(nlse_ctx *c) {
     cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result);
     if (c->h_div) cudaFreeHost(c->h_div);
     if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->side_stream) { cudaStreamSynchronize(c->side_stream); cudaStreamDestroy(c->side_stream); }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     c->stream_ref.reset();    // destroys the stream with its last user
     delete c;
 }
@@ -924,6 +974,15 @@ nlse_status nlse_step(nlse_ctx *c, double k, int64_t nsteps) {
     if ((st = check_step_args(c, k, nsteps))) return st;
     if (nsteps == 0) return NLSE_OK;
     if ((st = enqueue_halo_refresh(c))) return st;
+    if (c->persist1d) {
+        dispatch(c, [&](auto T, auto DIM, auto ORD, auto BCK) {
+            if constexpr (decltype(DIM)::value == 1)
+                launch_persist1d<decltype(T), decltype(ORD)::value, decltype(BCK)::value>(c, k, nsteps);
+            return 0;
+        });
+        enqueue_add_steps(c, nsteps);
+        return finish_steps(c, nsteps);
+    }
     int64_t done = 0;
     if (graphs_enabled(c, nsteps) && ensure_graph(c, k)) {
         for (; done + GRAPH_STEPS <= nsteps; done += GRAPH_STEPS)
@@ -1050,12 +1109,12 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     out->points = c->g.n;
     int per_stage = c->interior_kind == KK_GENERIC ? 1 : 2;
     if (c->dist && c->nranks > 1) per_stage += 1;
-    out->launches_per_step = 4 * per_stage;
+    out->launches_per_step = c->persist1d ? 0 : 4 * per_stage;   // 0: one launch per nlse_step call
     const int64_t cbytes = 2 * c->eb, rv = c->hasV ? c->eb : 0;
     out->min_bytes_per_step = (16 * cbytes + 4 * rv) * c->g.n;
     out->device_bytes = c->device_bytes;
     out->elem_bytes = c->eb;
-    snprintf(out->variant, sizeof out->variant, "%s", kKindName[c->interior_kind]);
+    snprintf(out->variant, sizeof out->variant, "%s", c->persist1d ? "rk4_1d_persistent" : kKindName[c->interior_kind]);
     out->rank = c->rank;
     out->nranks = c->nranks;
     out->z0 = c->z0;

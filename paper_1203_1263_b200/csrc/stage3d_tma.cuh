@@ -461,43 +461,32 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     if (z < ze) body(std::integral_constant<int, 1>(), z++);
 }
 
-// Persistent launch: gridDim.x CTAs (the resident count) walk the work items
-// w = blockIdx.x, blockIdx.x + gridDim.x, ... ordered z-chunk-major, then tile row, then
-// tile column.  All resident CTAs start together on consecutive tiles of one z chunk and
-// advance through z at the same rate, so the halo rows and columns a tile shares with its
-// neighbours are still in L2 when the neighbour loads them (with one CTA per tile in a
-// plain grid, CTAs start whenever a slot frees and drift apart by far more planes than
-// the ~25 us L2 residency at full HBM rate).
+// One CTA per work item (tile, z chunk); blockIdx.x enumerates the items z-chunk-major,
+// then tile row, then tile column, so the CTAs resident at any time cover whole bands of
+// consecutive tiles of one z chunk (their shared halo rows and columns are L2 hits).
+// Measured alternatives (r01g-j: a persistent grid drawing items from a counter, banded
+// tile orders) were not faster.
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
 __global__ void __launch_bounds__(32 * TYV, (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2)))
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
-            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int nchunks) {
+            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty) {
     using Cfg = T3Cfg<T, ORDER, P, TYV>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int ntiles = ntx * nty;
+    const int w = blockIdx.x;
+    const int c = w / ntiles, t = w - c * ntiles;
+    const int x0 = (t % ntx) * Cfg::TX, y0 = (t / ntx) * Cfg::TY;
     const int nz = int(A.g.nz);
     const int zlo = A.g.zf_lo ? 1 : 0, zhi = nz - (A.g.zf_hi ? 1 : 0);
+    const int zs = zlo + c * zchunk;
+    const int ze = min(zs + zchunk, zhi);
+    if (zs >= ze) return;
     const int nx = int(A.g.nx), ny = int(A.g.ny);
-    const int ntiles = ntx * nty;
-    const int total = ntiles * nchunks;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const int c = w / ntiles, t = w - c * ntiles;
-        const int x0 = (t % ntx) * Cfg::TX, y0 = (t / ntx) * Cfg::TY;
-        const int zs = zlo + c * zchunk;
-        const int ze = min(zs + zchunk, zhi);
-        if (zs < ze) {
-            // every owned and ring point in-plane interior -> branch-free path
-            const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
-            if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
-            else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
-        }
-        // retire this item's barriers before the next item re-initialises them
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned bar0 = smem_u32(smem_raw + Cfg::OFF_BAR);
-            for (int i = 0; i < Cfg::NS + Cfg::NP + 2; i++) mbar_inval(bar0 + 8 * i);
-        }
-    }
+    // every owned and ring point in-plane interior -> branch-free path
+    const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
+    if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
 }
 
 }  // namespace nlse

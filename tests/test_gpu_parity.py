@@ -45,7 +45,7 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
-    want = {"fast": {1: "stage1d_tile", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+    want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
             "generic": "stage_generic"}[kernel]
     if not (kernel == "fast" and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
         assert info["variant"] == want, info
