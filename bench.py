@@ -242,8 +242,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(local % ndev)
+        # torch.distributed is plumbing only here (handle all-gather, max-over-ranks timing;
+        # the halo exchange runs over peer memory).  NCCL with one GPU per rank; gloo when
+        # several ranks share a GPU (functional test of the N>1 path on a 1-GPU box).
+        backend = "nccl" if ndev >= world else "gloo"
+        dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     from paper_1203_1263_b200 import build
@@ -273,7 +278,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % max(1, torch.cuda.device_count())) as clk:
         # (1) the bench value: K steps, CUDA events on the library's stream around one nlse_step call
         e0.record(stream)
         sv.nlse_step(k, args.steps)
@@ -287,7 +292,7 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     timing = sv.nlse_get_timing()
@@ -323,7 +328,7 @@ def main():
         sv.nlse_get_psi(host)
         el = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([el], device="cuda")
+            t = torch.tensor([el], device="cuda" if backend == "nccl" else "cpu")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": npts * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": npts * 16 // args.steps,

@@ -185,27 +185,35 @@ struct T3Body {
     }
 };
 
+// The per-run constants the inner loop uses, read once into registers.
+template <typename T>
+struct HotC {
+    T ih2, c16h2, c112, a, s, kc;
+    __device__ __forceinline__ explicit HotC(const Consts<T> &c)
+        : ih2(c.ih2), c16h2(c.c16h2), c112(c.c112), a(c.a), s(c.s), kc(c.kc) {}
+};
+
 // F (fsplit) P:424-428 and the RK4 stage combine (RK4_GPU) P:495-519 at one point.
 template <typename T, int STAGE>
-__device__ __forceinline__ void t3_finish(const StageArgs<T> &A, int64_t q, int z, cplx<T> yc, cplx<T> L,
-                                          cplx<T> psi, cplx<T> kt, T v) {
+__device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &hc, int64_t q, int z, cplx<T> yc,
+                                          cplx<T> L, cplx<T> psi, cplx<T> kt, T v) {
     using C = cplx<T>;
     const T rho = (yc.x * yc.x) + (yc.y * yc.y);
-    const T sr = A.c.s * rho;
-    T fr = (-(A.c.a * L.y)) - (sr * yc.y);
-    T fi = (A.c.a * L.x) + (sr * yc.x);
+    const T sr = hc.s * rho;
+    T fr = (-(hc.a * L.y)) - (sr * yc.y);
+    T fi = (hc.a * L.x) + (sr * yc.x);
     if (A.V) { fr = fr + (v * yc.y); fi = fi - (v * yc.x); }
     C F; F.x = fr; F.y = fi;
     if (STAGE == 1) {
         A.K[q] = F;
-        store_out(A, q, z, cadd(yc, cscale(A.c.kc, F)));
+        store_out(A, q, z, cadd(yc, cscale(hc.kc, F)));
     } else if (STAGE == 4) {
-        const C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
+        const C r4 = cadd(psi, cscale(hc.kc, cadd(kt, F)));
         store_out(A, q, z, r4);
         if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
         A.K[q] = cadd(kt, cscale(T(2), F));
-        store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
+        store_out(A, q, z, cadd(psi, cscale(hc.kc, F)));
     }
 }
 
@@ -218,6 +226,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     using B = T3Body<T, ORDER, BC, STAGE, P, TYV, EDGE>;
     constexpr int H = Cfg::H, TX = Cfg::TX, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
     const B b{A, sm, x0, y0};
+    const HotC<T> hc(A.c);
     const Grid &g = A.g;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int nz = int(g.nz);
@@ -317,8 +326,8 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
                 C acc = csub(cadd(Y0[-1], Y0[1]), y2);
                 acc = cadd(acc, csub(cadd(Y0[-PX], Y0[PX]), y2));
                 acc = cadd(acc, csub(cadd(ym, yp), y2));
-                const C L = cscale(A.c.ih2, acc);
-                t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yc, L, psi, kt, v);
+                const C L = cscale(hc.ih2, acc);
+                t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, yc, L, psi, kt, v);
             }
             ym = yc; yc = yp;
             sm1 = s0; s0 = s1;
@@ -406,7 +415,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             C acc = csub(px1, y2);
             acc = cadd(acc, csub(py1, y2));
             acc = cadd(acc, csub(cadd(yq[I0], yz2), y2));
-            dn = cscale(A.c.ih2, acc);
+            dn = cscale(hc.ih2, acc);
         }
         b.dslot(d1s)[downo] = dn;
         if (ring) {
@@ -424,7 +433,8 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         mbar_arrive(cbar0 + 8 * ((j + 1) & 1));            // phase j+1: D(z+1) written
         // 2SHOC step 2, grouping of DESIGN.md §3.1: the parts that need no
         // neighbour D first, then wait for phase j (D(z) of the whole tile + ring)
-        const C y4 = cscale(T(4), yq[I0]);
+        const C y2c = cadd(yq[I0], yq[I0]);
+        const C y4 = cadd(y2c, y2c);                        // = 4 Y exactly (powers of two)
         const C pxa = cadd(Y0[-PX - 1], Y0[-PX + 1]);
         const C pxb = cadd(Y0[PX - 1], Y0[PX + 1]);
         const C exy = csub(cadd(pxa, pxb), y4);
@@ -440,8 +450,8 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             const C *Dz = b.dslot(d0s) + downo;
             const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dq[I0], dn));
             const C td = csub(sd, cscale(T(10), dq[I1]));
-            const C L = csub(cscale(A.c.c16h2, E), cscale(A.c.c112, td));
-            t3_finish<T, STAGE>(A, int64_t(z) * g.sz + qrow, z, yq[I0], L, psi, kt, v);
+            const C L = csub(cscale(hc.c16h2, E), cscale(hc.c112, td));
+            t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, yq[I0], L, psi, kt, v);
         }
         // queue update (the slots of plane z-1 become those of plane z+2) and ring rotation
         dq[I2] = dn; pxq[I2] = px1; pyq[I2] = py1; yq[I2] = yz2;
