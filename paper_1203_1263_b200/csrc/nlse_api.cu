@@ -266,8 +266,13 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
         attr_set = true;
     }
     const int64_t items = int64_t(gx) * gy * gz;
+    static const bool force_edge = [] {      // debug / measurement: every tile on the face-aware path
+        const char *e = getenv("NLSE_FORCE_EDGE");
+        return e && e[0] == '1';
+    }();
     stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
-        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy));
+        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
+        force_edge ? 1 : 0);
 }
 
 template <typename T, int ORDER, int BC, int STAGE>

@@ -480,7 +480,7 @@ template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
 __global__ void __launch_bounds__(32 * TYV, (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2)))
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
-            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty) {
+            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge) {
     using Cfg = T3Cfg<T, ORDER, P, TYV>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int ntiles = ntx * nty;
@@ -494,7 +494,7 @@ stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUte
     if (zs >= ze) return;
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     // every owned and ring point in-plane interior -> branch-free path
-    const bool edge = !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
+    const bool edge = force_edge || !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
     if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
     else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
 }

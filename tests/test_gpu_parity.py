@@ -228,3 +228,41 @@ def test_divergence_step_index_with_graphs():
             assert e.value.status == NLSE_ERR_DIVERGED
             msgs.append(str(e.value))
     assert msgs[0] == msgs[1], msgs
+
+
+def test_config5_gpe3d_full_size_sampled():
+    """configs[4] at full size (1024^3 fp64 + V, 2SHOC, MSD) in the launch configuration bench.py
+    times, 2 RK4 steps: sampled outputs vs the oracle, bit for bit.  A point's value after n steps
+    depends only on Psi within 4 stages x 2 points x n of it, so the oracle runs on a sub-block
+    around each sample (sub-blocks that touch the domain boundary keep the true boundary) and is
+    compared on the part of the sub-block at least 8n points away from its artificial edges."""
+    import oracle
+    from paper_1203_1263_b200.nlse import Solver
+    n, nsteps, m = 1024, 2, 16                     # margin m = 8 * nsteps
+    cfg = inputs.config("gpe3d")
+    psi, V = inputs.gpe3d_fill(n)
+    with Solver(cfg["dims"], cfg["h"], a=1.0, s=-1.0, V=V, bc="msd", scheme="2shoc", precision="fp64") as sv:
+        assert sv.nlse_get_info()["variant"] == "stage3d_tma"
+        sv.nlse_set_psi(psi)
+        sv.nlse_step(cfg["k"], nsteps)
+        got = sv.nlse_get_psi()
+    p_or = lambda d: oracle.Problem(d, cfg["h"], a=1.0, s=-1.0, bc="msd", scheme="2shoc")
+    half = 12
+    # (z, y, x) sample centres: interior, the corner, an x face, the top z face, a y edge
+    for cz, cy, cx in [(511, 300, 700), (0, 0, 0), (600, 400, 0), (1023, 512, 511), (200, 1023, 900)]:
+        lo = [max(0, c - half - m) for c in (cz, cy, cx)]
+        hi = [min(n, c + half + m + 1) for c in (cz, cy, cx)]
+        sl = tuple(slice(a, b) for a, b in zip(lo, hi))
+        sub = np.ascontiguousarray(psi[sl])
+        ref = oracle.step(p_or(tuple(reversed(sub.shape))), sub, cfg["k"], nsteps, np.ascontiguousarray(V[sl]))
+        # compare where the sub-block edge is a true domain boundary or at least m away
+        keep = []
+        for ax in range(3):
+            a0 = 0 if lo[ax] == 0 else m
+            a1 = sub.shape[ax] if hi[ax] == n else sub.shape[ax] - m
+            keep.append(slice(a0, a1))
+        keep = tuple(keep)
+        g = np.ascontiguousarray(got[sl][keep])
+        r = np.ascontiguousarray(ref[keep].astype(np.complex128))
+        assert g.size > 0
+        assert np.array_equal(g.view(np.uint64), r.view(np.uint64)), (cz, cy, cx, rel_l2(g, r))
