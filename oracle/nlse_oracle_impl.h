@@ -28,6 +28,14 @@ typedef struct {
     REAL eps2;   /* MSD division guard    reading R-MSD-GUARD */
 } FN(oracle_consts);
 
+/* Fused multiply-add, one IEEE rounding (C99 fma / fmaf): the canonical DAG contracts a
+ * product into a following add at the positions listed in DESIGN.md reading R-ASSOC
+ * (the CUDA side uses the same explicit fused operations, so both stay bit-identical). */
+static REAL FN(fmar)(REAL a, REAL b, REAL c)
+{
+    return sizeof(REAL) == 8 ? (REAL)fma((double)a, (double)b, (double)c) : (REAL)fmaf((float)a, (float)b, (float)c);
+}
+
 static FN(oracle_consts) FN(make_consts)(const oracle_problem *p)
 {
     FN(oracle_consts) c;
@@ -176,7 +184,7 @@ static void FN(l_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
     if (p->ndim == 1) {
         for (long i = 1; i < nx - 1; i++)
             l[i] = (p->order == 2) ? d[i]
-                 : (c->c76 * d[i]) - (c->c112 * (d[i - sx] + d[i + sx]));
+                 : FN(fmar)(c->c76, d[i], -(c->c112 * (d[i - sx] + d[i + sx])));
     } else if (p->ndim == 2) {
         for (long j = 1; j < ny - 1; j++)
             for (long i = 1; i < nx - 1; i++) {
@@ -184,8 +192,8 @@ static void FN(l_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
                 if (p->order == 2) { l[q] = d[q]; continue; }
                 REAL y4 = four * y[q];
                 REAL cxy = ((y[q - sx - sy] + y[q + sx - sy]) + (y[q - sx + sy] + y[q + sx + sy])) - y4;
-                REAL td = ((d[q - sx] + d[q + sx]) + (d[q - sy] + d[q + sy])) - (twelve * d[q]);
-                l[q] = (c->c16h2 * cxy) - (c->c112 * td);
+                REAL td = FN(fmar)(-twelve, d[q], (d[q - sx] + d[q + sx]) + (d[q - sy] + d[q + sy]));
+                l[q] = FN(fmar)(c->c16h2, cxy, -(c->c112 * td));
             }
     } else {
         for (long k = 1; k < nz - 1; k++)
@@ -198,9 +206,9 @@ static void FN(l_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
                     REAL exz = ((y[q - sx - sz] + y[q + sx - sz]) + (y[q - sx + sz] + y[q + sx + sz])) - y4;
                     REAL eyz = ((y[q - sy - sz] + y[q + sy - sz]) + (y[q - sy + sz] + y[q + sy + sz])) - y4;
                     REAL e = (exy + exz) + eyz;
-                    REAL td = (((d[q - sx] + d[q + sx]) + (d[q - sy] + d[q + sy]))
-                               + (d[q - sz] + d[q + sz])) - (ten * d[q]);
-                    l[q] = (c->c16h2 * e) - (c->c112 * td);
+                    REAL td = FN(fmar)(-ten, d[q], ((d[q - sx] + d[q + sx]) + (d[q - sy] + d[q + sy]))
+                                                   + (d[q - sz] + d[q + sz]));
+                    l[q] = FN(fmar)(c->c16h2, e, -(c->c112 * td));
                 }
     }
 }
@@ -214,11 +222,11 @@ static void FN(f_point)(const FN(oracle_consts) *c, REAL yr, REAL yi, REAL lr, R
 {
     REAL rho = (yr * yr) + (yi * yi);
     REAL sr = c->s * rho;
-    REAL r = (-(c->a * li)) - (sr * yi);
-    REAL m = (c->a * lr) + (sr * yr);
+    REAL r = FN(fmar)(-c->a, li, -(sr * yi));
+    REAL m = FN(fmar)(c->a, lr, sr * yr);
     if (V) {
-        r = r + (V[q] * yi);
-        m = m - (V[q] * yr);
+        r = FN(fmar)(V[q], yi, r);
+        m = FN(fmar)(-V[q], yr, m);
     }
     *fr = r;
     *fi = m;
@@ -330,17 +338,17 @@ int FN(oracle_step)(const oracle_problem *p, const REAL *V, REAL *re, REAL *im,
 
     for (long step = 0; step < nsteps; step++) {
         /* 1) */ FN(rhs)(p, &c, V, re, im, ktr, kti, dr, di, lr, li);
-        /* 2) */ for (long q = 0; q < n; q++) { ptr[q] = re[q] + (k2 * ktr[q]); pti[q] = im[q] + (k2 * kti[q]); }
+        /* 2) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k2, ktr[q], re[q]); pti[q] = FN(fmar)(k2, kti[q], im[q]); }
         /* 3) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
-        /* 4) */ for (long q = 0; q < n; q++) { ktr[q] = ktr[q] + (two * kmr[q]); kti[q] = kti[q] + (two * kmi[q]); }
-        /* 5) */ for (long q = 0; q < n; q++) { ptr[q] = re[q] + (k2 * kmr[q]); pti[q] = im[q] + (k2 * kmi[q]); }
+        /* 4) */ for (long q = 0; q < n; q++) { ktr[q] = FN(fmar)(two, kmr[q], ktr[q]); kti[q] = FN(fmar)(two, kmi[q], kti[q]); }
+        /* 5) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k2, kmr[q], re[q]); pti[q] = FN(fmar)(k2, kmi[q], im[q]); }
         /* 6) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
-        /* 7) */ for (long q = 0; q < n; q++) { ktr[q] = ktr[q] + (two * kmr[q]); kti[q] = kti[q] + (two * kmi[q]); }
-        /* 8) */ for (long q = 0; q < n; q++) { ptr[q] = re[q] + (k1 * kmr[q]); pti[q] = im[q] + (k1 * kmi[q]); }
+        /* 7) */ for (long q = 0; q < n; q++) { ktr[q] = FN(fmar)(two, kmr[q], ktr[q]); kti[q] = FN(fmar)(two, kmi[q], kti[q]); }
+        /* 8) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k1, kmr[q], re[q]); pti[q] = FN(fmar)(k1, kmi[q], im[q]); }
         /* 9) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
         /* 10) */ for (long q = 0; q < n; q++) {
-            re[q] = re[q] + (k6 * (ktr[q] + kmr[q]));
-            im[q] = im[q] + (k6 * (kti[q] + kmi[q]));
+            re[q] = FN(fmar)(k6, ktr[q] + kmr[q], re[q]);
+            im[q] = FN(fmar)(k6, kti[q] + kmi[q], im[q]);
         }
     }
     free(w);

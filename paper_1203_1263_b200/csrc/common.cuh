@@ -26,6 +26,15 @@ template <typename C, typename T> __device__ __forceinline__ C cscale(T s, C a) 
 
 template <typename C> __device__ __forceinline__ C ldg_c(const C *p) { return __ldg(p); }
 
+// Fused multiply-add with one IEEE rounding, at the positions DESIGN.md §3.1 (R-ASSOC)
+// fixes (the oracle uses C99 fma / fmaf at the same positions).
+__device__ __forceinline__ double tfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float tfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+template <typename C, typename T> __device__ __forceinline__ C cfma(T s, C a, C b) {
+    C r; r.x = tfma(s, a.x, b.x); r.y = tfma(s, a.y, b.y); return r;
+}
+template <typename C> __device__ __forceinline__ C cneg(C a) { C r; r.x = -a.x; r.y = -a.y; return r; }
+
 // Per-run constants, evaluated in double on the host from the user's doubles and
 // rounded once to T (reading R-CONST).
 template <typename T> struct Consts {
@@ -87,11 +96,12 @@ __device__ __forceinline__ void store_out(const StageArgs<T> &A, int64_t q, int6
     if (A.peer_hi && k >= A.g.nz - A.wsend) A.peer_hi[q] = v;
 }
 
-// RK4 stage combine at one point, (RK4_GPU) P:495-519 / (RK4) P:164-180:
-//   S1: K = F;      out = Psi + (k/2) F
-//   S2: K = K + 2F; out = Psi + (k/2) F
-//   S3: K = K + 2F; out = Psi + k F
-//   S4:             out = Psi + (k/6)(K + F)
+// RK4 stage combine at one point, (RK4_GPU) P:495-519 / (RK4) P:164-180 (fused
+// multiply-adds, R-ASSOC):
+//   S1: K = F;            out = fma(k/2, F, Psi)
+//   S2: K = fma(2, F, K); out = fma(k/2, F, Psi)
+//   S3: K = fma(2, F, K); out = fma(k, F, Psi)
+//   S4:                   out = fma(k/6, K + F, Psi)
 // kz = local plane of q (for the neighbour stores; 0 in 1D / 2D).
 template <int STAGE, typename T>
 __device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, int64_t kz, cplx<T> F, cplx<T> psi) {
@@ -99,14 +109,14 @@ __device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, int
     const T two = T(2);
     if (STAGE == 1) {
         A.K[q] = F;
-        store_out(A, q, kz, cadd(psi, cscale(A.c.kc, F)));
+        store_out(A, q, kz, cfma(A.c.kc, F, psi));
     } else if (STAGE == 2 || STAGE == 3) {
         C k = A.K[q];
-        A.K[q] = cadd(k, cscale(two, F));
-        store_out(A, q, kz, cadd(psi, cscale(A.c.kc, F)));
+        A.K[q] = cfma(two, F, k);
+        store_out(A, q, kz, cfma(A.c.kc, F, psi));
     } else {
         C k = A.K[q];
-        C r = cadd(psi, cscale(A.c.kc, cadd(k, F)));
+        C r = cfma(A.c.kc, cadd(k, F), psi);
         store_out(A, q, kz, r);
         if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(A.diverged, *A.step_base + A.step);
     }

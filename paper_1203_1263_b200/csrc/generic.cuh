@@ -97,14 +97,14 @@ struct PointEval {
         const C d0 = D_int(q);
         if (DIM == 1) {
             C dm = D_any(i - 1, j, k), dp = D_any(i + 1, j, k);
-            return csub(cscale(c.c76, d0), cscale(c.c112, cadd(dm, dp)));
+            return cfma(c.c76, d0, cneg(cscale(c.c112, cadd(dm, dp))));
         }
         const C y4 = cscale(T(4), y(q));
         if (DIM == 2) {
             C cxy = csub(cadd(cadd(y(q - 1 - g.sy), y(q + 1 - g.sy)), cadd(y(q - 1 + g.sy), y(q + 1 + g.sy))), y4);
             C sd = cadd(cadd(D_any(i - 1, j, k), D_any(i + 1, j, k)), cadd(D_any(i, j - 1, k), D_any(i, j + 1, k)));
-            C td = csub(sd, cscale(T(12), d0));
-            return csub(cscale(c.c16h2, cxy), cscale(c.c112, td));
+            C td = cfma(T(-12), d0, sd);
+            return cfma(c.c16h2, cxy, cneg(cscale(c.c112, td)));
         }
         C exy = csub(cadd(cadd(y(q - 1 - g.sy), y(q + 1 - g.sy)), cadd(y(q - 1 + g.sy), y(q + 1 + g.sy))), y4);
         C exz = csub(cadd(cadd(y(q - 1 - g.sz), y(q + 1 - g.sz)), cadd(y(q - 1 + g.sz), y(q + 1 + g.sz))), y4);
@@ -112,20 +112,20 @@ struct PointEval {
         C e = cadd(cadd(exy, exz), eyz);
         C sd = cadd(cadd(cadd(D_any(i - 1, j, k), D_any(i + 1, j, k)), cadd(D_any(i, j - 1, k), D_any(i, j + 1, k))),
                     cadd(D_any(i, j, k - 1), D_any(i, j, k + 1)));
-        C td = csub(sd, cscale(T(10), d0));
-        return csub(cscale(c.c16h2, e), cscale(c.c112, td));
+        C td = cfma(T(-10), d0, sd);
+        return cfma(c.c16h2, e, cneg(cscale(c.c112, td)));
     }
 
     // Interior F, (fsplit) P:424-428.
     __device__ __forceinline__ C F_from(int64_t q, C yq, C L) const {
         T rho = (yq.x * yq.x) + (yq.y * yq.y);
         T sr = c.s * rho;
-        T r = (-(c.a * L.y)) - (sr * yq.y);
-        T m = (c.a * L.x) + (sr * yq.x);
+        T r = tfma(-c.a, L.y, -(sr * yq.y));
+        T m = tfma(c.a, L.x, sr * yq.x);
         if (V) {
             T vq = v(q);
-            r = r + (vq * yq.y);
-            m = m - (vq * yq.x);
+            r = tfma(vq, yq.y, r);
+            m = tfma(-vq, yq.x, m);
         }
         C f; f.x = r; f.y = m;
         return f;

@@ -245,13 +245,29 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     const int64_t mz = A.g.nz - A.g.zf_lo - A.g.zf_hi;
     const unsigned gx = unsigned((nx + Cfg::TX - 1) / Cfg::TX);
     const unsigned gy = unsigned((ny + Cfg::TY - 1) / Cfg::TY);
-    // z chunks of 128 planes (L2 locality of the persistent walk, see stage3d_tma), fewer
-    // for small grids so that there are about two items per resident CTA
+    // z chunks: at most 128 planes (L2 locality of neighbouring tiles, r01e), and the
+    // chunk count that minimises (waves of resident CTAs) x (planes per chunk + the ~4-plane
+    // prologue), so that small grids fill the GPU in whole waves
     const int64_t cols = int64_t(gx) * gy;
-    const int64_t resident = 148 * (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2));
-    const int64_t want = (2 * resident + cols - 1) / cols;
-    int64_t zchunk = std::min<int64_t>(128, (mz + want - 1) / want);
-    if (zchunk < 8) zchunk = 8;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+                                                      Cfg::NT, Cfg::SMEM);
+        if (per_sm < 1) per_sm = 1;
+    }
+    static int nsm = 0;
+    if (!nsm && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) nsm = 148;
+    const int64_t resident = int64_t(nsm) * per_sm;
+    int64_t zchunk = mz, best = -1;
+    for (int64_t nzc = (mz + 127) / 128; nzc <= mz; nzc++) {
+        const int64_t ch = (mz + nzc - 1) / nzc;
+        const int64_t waves = (cols * nzc + resident - 1) / resident;
+        const int64_t cost = waves * (ch + 4);
+        if (best < 0 || cost < best) { best = cost; zchunk = ch; }
+        if (ch <= 4) break;
+    }
     static const int64_t env_chunk = [] {
         const char *e = getenv("NLSE_ZCHUNK");
         return e ? std::atoll(e) : int64_t(0);
@@ -259,12 +275,6 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     if (env_chunk > 0) zchunk = env_chunk;
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        attr_set = true;
-    }
     const int64_t items = int64_t(gx) * gy * gz;
     static const bool force_edge = [] {      // debug / measurement: every tile on the face-aware path
         const char *e = getenv("NLSE_FORCE_EDGE");

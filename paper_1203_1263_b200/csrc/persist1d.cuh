@@ -66,9 +66,9 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
     auto f_of = [&](const Consts<T> &c, int i, C y, C L) -> C {
         const T rho = (y.x * y.x) + (y.y * y.y);
         const T sr = c.s * rho;
-        T fr = (-(c.a * L.y)) - (sr * y.y);
-        T fi = (c.a * L.x) + (sr * y.x);
-        if (hasV) { fr = fr + (Vs[i] * y.y); fi = fi - (Vs[i] * y.x); }
+        T fr = tfma(-c.a, L.y, -(sr * y.y));
+        T fi = tfma(c.a, L.x, sr * y.x);
+        if (hasV) { fr = tfma(Vs[i], y.y, fr); fi = tfma(-Vs[i], y.x, fi); }
         C F; F.x = fr; F.y = fi;
         return F;
     };
@@ -82,14 +82,14 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
             auto combine = [&](int i, C F) {
                 if (stage == 1) {
                     Ks[i] = F;
-                    Out[i] = cadd(Y[i], cscale(c.kc, F));
+                    Out[i] = cfma(c.kc, F, Y[i]);
                 } else if (stage == 4) {
-                    const C r = cadd(Ps[i], cscale(c.kc, cadd(Ks[i], F)));
+                    const C r = cfma(c.kc, cadd(Ks[i], F), Ps[i]);
                     Out[i] = r;
                     if (!(isfinite(r.x) && isfinite(r.y))) atomicMin(P.diverged, *P.step_base + int(step));
                 } else {
-                    Ks[i] = cadd(Ks[i], cscale(T(2), F));
-                    Out[i] = cadd(Ps[i], cscale(c.kc, F));
+                    Ks[i] = cfma(T(2), F, Ks[i]);
+                    Out[i] = cfma(c.kc, F, Ps[i]);
                 }
             };
             // (1) 2SHOC step 1 with boundary D from the Laplacian form of the BC
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
             for (int i = 1 + threadIdx.x; i < n - 1; i += P1_THREADS) {
                 C L;
                 if (ORDER == ORDER_CD) L = d_int(c, Y, i);
-                else L = csub(cscale(c.c76, Ds[i]), cscale(c.c112, cadd(Ds[i - 1], Ds[i + 1])));
+                else L = cfma(c.c76, Ds[i], cneg(cscale(c.c112, cadd(Ds[i - 1], Ds[i + 1]))));
                 const C F = f_of(c, i, Y[i], L);
                 Fs[i] = F;
                 combine(i, F);

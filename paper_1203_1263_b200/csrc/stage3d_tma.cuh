@@ -200,20 +200,20 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &
     using C = cplx<T>;
     const T rho = (yc.x * yc.x) + (yc.y * yc.y);
     const T sr = hc.s * rho;
-    T fr = (-(hc.a * L.y)) - (sr * yc.y);
-    T fi = (hc.a * L.x) + (sr * yc.x);
-    if (A.V) { fr = fr + (v * yc.y); fi = fi - (v * yc.x); }
+    T fr = tfma(-hc.a, L.y, -(sr * yc.y));
+    T fi = tfma(hc.a, L.x, sr * yc.x);
+    if (A.V) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
     C F; F.x = fr; F.y = fi;
     if (STAGE == 1) {
         A.K[q] = F;
-        store_out(A, q, z, cadd(yc, cscale(hc.kc, F)));
+        store_out(A, q, z, cfma(hc.kc, F, yc));
     } else if (STAGE == 4) {
-        const C r4 = cadd(psi, cscale(hc.kc, cadd(kt, F)));
+        const C r4 = cfma(hc.kc, cadd(kt, F), psi);
         store_out(A, q, z, r4);
         if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
-        A.K[q] = cadd(kt, cscale(T(2), F));
-        store_out(A, q, z, cadd(psi, cscale(hc.kc, F)));
+        A.K[q] = cfma(T(2), F, kt);
+        store_out(A, q, z, cfma(hc.kc, F, psi));
     }
 }
 
@@ -449,8 +449,8 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         if (out_ok) {
             const C *Dz = b.dslot(d0s) + downo;
             const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dq[I0], dn));
-            const C td = csub(sd, cscale(T(10), dq[I1]));
-            const C L = csub(cscale(hc.c16h2, E), cscale(hc.c112, td));
+            const C td = cfma(T(-10), dq[I1], sd);
+            const C L = cfma(hc.c16h2, E, cneg(cscale(hc.c112, td)));
             t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, yq[I0], L, psi, kt, v);
         }
         // queue update (the slots of plane z-1 become those of plane z+2) and ring rotation

@@ -167,20 +167,20 @@ __device__ __forceinline__ void finish_point(const StageArgs<T> &A, int64_t q, i
     using C = cplx<T>;
     T rho = (yc.x * yc.x) + (yc.y * yc.y);
     T sr = A.c.s * rho;
-    T fr = (-(A.c.a * L.y)) - (sr * yc.y);
-    T fi = (A.c.a * L.x) + (sr * yc.x);
-    if (A.V) { fr = fr + (v * yc.y); fi = fi - (v * yc.x); }
+    T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
+    T fi = tfma(A.c.a, L.x, sr * yc.x);
+    if (A.V) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
     C F; F.x = fr; F.y = fi;
     if (STAGE == 1) {
         A.K[q] = F;
-        store_out(A, q, z, cadd(yc, cscale(A.c.kc, F)));
+        store_out(A, q, z, cfma(A.c.kc, F, yc));
     } else if (STAGE == 4) {
-        C r4 = cadd(psi, cscale(A.c.kc, cadd(kt, F)));
+        C r4 = cfma(A.c.kc, cadd(kt, F), psi);
         store_out(A, q, z, r4);
         if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
-        A.K[q] = cadd(kt, cscale(T(2), F));
-        store_out(A, q, z, cadd(psi, cscale(A.c.kc, F)));
+        A.K[q] = cfma(T(2), F, kt);
+        store_out(A, q, z, cfma(A.c.kc, F, psi));
     }
 }
 
@@ -396,8 +396,8 @@ stage3d_stream(StageArgs<T> A, int zchunk) {
             const C dyb = (r < RY - 1) ? d0[r + 1] : k.Ds(dsl, tx, ly + 1);
             const C sd = cadd(cadd(cadd(k.Ds(dsl, tx - 1, ly), k.Ds(dsl, tx + 1, ly)), cadd(dya, dyb)),
                               cadd(dm[r], dn[r]));
-            const C td = csub(sd, cscale(T(10), d0[r]));
-            const C L = csub(cscale(A.c.c16h2, E), cscale(A.c.c112, td));
+            const C td = cfma(T(-10), d0[r], sd);
+            const C L = cfma(A.c.c16h2, E, cneg(cscale(A.c.c112, td)));
             finish_point<T, STAGE>(A, zo + qrow[r], z, yc, L, psi[r], kt[r], v[r]);
         }
         // (4) rotate the register queues and the slots

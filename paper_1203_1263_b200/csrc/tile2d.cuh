@@ -112,18 +112,18 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
             const C cxy = csub(cadd(pxa, pxb), y4);
             const C *Dp = ds + (ly + 1) * DPX + (lx + 1);
             const C sd = cadd(cadd(Dp[-1], Dp[1]), cadd(Dp[-DPX], Dp[DPX]));
-            const C td = csub(sd, cscale(T(12), Dp[0]));
-            L = csub(cscale(A.c.c16h2, cxy), cscale(A.c.c112, td));
+            const C td = cfma(T(-12), Dp[0], sd);
+            L = cfma(A.c.c16h2, cxy, cneg(cscale(A.c.c112, td)));
         }
         // F (fsplit) P:424-428
         const T rho = (yc.x * yc.x) + (yc.y * yc.y);
         const T sr = A.c.s * rho;
-        T fr = (-(A.c.a * L.y)) - (sr * yc.y);
-        T fi = (A.c.a * L.x) + (sr * yc.x);
+        T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
+        T fi = tfma(A.c.a, L.x, sr * yc.x);
         if (A.V) {
             const T v = __ldg(A.V + q);
-            fr = fr + (v * yc.y);
-            fi = fi - (v * yc.x);
+            fr = tfma(v, yc.y, fr);
+            fi = tfma(-v, yc.x, fi);
         }
         C F; F.x = fr; F.y = fi;
         const C psi = (STAGE == 1) ? yc : A.Psi[q];
