@@ -86,7 +86,21 @@ template <typename T> struct StageArgs {
     // neighbour's copy of local point q; nullptr on a global face or on one GPU.
     cplx<T> *peer_lo, *peer_hi;
     int wsend;
+    // MSD, 3D TMA path: the interior kernel also stores F at the points b' that the boundary
+    // points take their time derivative from ((msd) P:331-335): fz = planes 1 and nz-2
+    // (2 x nx*ny), fp = the ring of points one in from the x/y faces of every owned plane
+    // (nz x per2, indexed by shell_u).  nullptr: the boundary kernel recomputes F(b').
+    cplx<T> *fz, *fp;
+    int per2;
 };
+
+// Index of an in-plane point one step in from the x/y faces (nx, ny >= 5), in the order:
+// row j = 1, row j = ny-2, then columns i = 1 / i = nx-2 for j = 2 .. ny-3.
+__host__ __device__ __forceinline__ int shell_u(int i, int j, int nx, int ny) {
+    if (j == 1) return i - 1;
+    if (j == ny - 2) return (nx - 2) + (i - 1);
+    return 2 * (nx - 2) + 2 * (j - 2) + (i == nx - 2 ? 1 : 0);
+}
 
 // Store one stage output value at local point q of plane k (and into the neighbours' ghosts).
 template <typename T>

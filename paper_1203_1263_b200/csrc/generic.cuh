@@ -184,35 +184,41 @@ __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
 // owns (plane 0 if zf_lo, plane nz-1 if zf_hi), then the perimeter of every other
 // owned plane.
 template <int DIM>
-__device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t, int64_t &i, int64_t &j, int64_t &k) {
+__device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i, int64_t &j, int64_t &k) {
+    // 32-bit index arithmetic (64-bit division is a long software sequence on the GPU); the
+    // launch checks that the boundary count and a face fit in 31 bits
+    const unsigned nx = unsigned(g.nx), ny = unsigned(g.ny);
+    unsigned t = unsigned(t64);
     if (DIM == 1) {
-        if (t >= 2) return false;
+        if (t >= 2u) return false;
         i = t ? g.nx - 1 : 0; j = 0; k = 0;
         return true;
     }
-    const int64_t per = 2 * g.nx + 2 * (g.ny - 2);    // perimeter of one xy plane
-    auto perim = [&](int64_t u, int64_t &ii, int64_t &jj) {
-        if (u < g.nx) { ii = u; jj = 0; }
-        else if (u < 2 * g.nx) { ii = u - g.nx; jj = g.ny - 1; }
-        else { int64_t v = u - 2 * g.nx; ii = (v & 1) ? g.nx - 1 : 0; jj = 1 + (v >> 1); }
+    const unsigned per = 2u * nx + 2u * (ny - 2u);    // perimeter of one xy plane
+    auto perim = [&](unsigned u, int64_t &ii, int64_t &jj) {
+        if (u < nx) { ii = u; jj = 0; }
+        else if (u < 2u * nx) { ii = u - nx; jj = ny - 1u; }
+        else { const unsigned v = u - 2u * nx; ii = (v & 1u) ? nx - 1u : 0; jj = 1u + (v >> 1); }
     };
     if (DIM == 2) {
         if (t >= per) return false;
         perim(t, i, j); k = 0;
         return true;
     }
-    const int64_t face = g.nx * g.ny;
-    const int nf = g.zf_lo + g.zf_hi;
+    const unsigned face = nx * ny;
+    const unsigned nf = unsigned(g.zf_lo + g.zf_hi);
     if (t < nf * face) {
         k = (g.zf_lo && t < face) ? 0 : g.nz - 1;
-        int64_t u = (t < face) ? t : t - face;
-        i = u % g.nx; j = u / g.nx;
+        const unsigned u = (t < face) ? t : t - face;
+        const unsigned jj = u / nx;
+        i = u - jj * nx; j = jj;
         return true;
     }
     t -= nf * face;
-    if (t >= per * (g.nz - nf)) return false;
-    k = g.zf_lo + t / per;
-    perim(t % per, i, j);
+    const unsigned kk = t / per;
+    if (kk >= unsigned(g.nz) - nf) return false;
+    k = int64_t(g.zf_lo) + kk;
+    perim(t - kk * per, i, j);
     return true;
 }
 
@@ -234,6 +240,37 @@ __global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_bnd(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
+    rk_combine<STAGE, T>(A, q, k, F, psi);
+}
+
+// 3D MSD boundary points with F(b') taken from what the interior kernel stored (A.fz /
+// A.fp), instead of recomputing the two-step Laplacian at b': (msd) P:331-335,
+// F_b = i Im(F_b'/Y_b') Y_b, same arithmetic as PointEval::F_bnd.
+template <typename T, int STAGE>
+__global__ void __launch_bounds__(256) stage_boundary_msd_fb(StageArgs<T> A) {
+    using C = cplx<T>;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t i, j, k;
+    if (!bnd_point<3>(A.g, t, i, j, k)) return;
+    const int nx = int(A.g.nx), ny = int(A.g.ny);
+    const int i1 = i == 0 ? 1 : (i == nx - 1 ? nx - 2 : int(i));
+    const int j1 = j == 0 ? 1 : (j == ny - 1 ? ny - 2 : int(j));
+    const bool zlo = A.g.zf_lo && k == 0, zhi = A.g.zf_hi && k == A.g.nz - 1;
+    const int64_t k1 = zlo ? 1 : (zhi ? A.g.nz - 2 : k);
+    C f1;
+    if (zlo) f1 = A.fz[int64_t(j1) * nx + i1];
+    else if (zhi) f1 = A.fz[int64_t(nx) * ny + int64_t(j1) * nx + i1];
+    else f1 = A.fp[k * A.per2 + shell_u(i1, j1, nx, ny)];
+    const int64_t q = k * A.g.sz + j * A.g.sy + i;
+    const C y1 = A.Y[k1 * A.g.sz + int64_t(j1) * A.g.sy + i1];
+    const C yb = A.Y[q];
+    const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+    T m = T(0);
+    if (!(rho1 < A.c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
+    C F;
+    F.x = -(m * yb.y);
+    F.y = m * yb.x;
+    const C psi = (STAGE == 1) ? yb : A.Psi[q];
     rk_combine<STAGE, T>(A, q, k, F, psi);
 }
 

@@ -76,6 +76,8 @@ struct nlse_ctx {
     void *alloc[3] = {nullptr, nullptr, nullptr};
     void *buf[3] = {nullptr, nullptr, nullptr};
     void *K = nullptr, *V = nullptr;
+    void *fz = nullptr, *fp = nullptr;   // MSD 3D TMA path: stored F(b') (see StageArgs)
+    int per2 = 0;
     int *d_div = nullptr;
     int *h_div = nullptr;            // pinned
     int *d_steps = nullptr;          // device counter of completed steps (divergence report)
@@ -303,7 +305,7 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
     // 3D: the boundary kernel (disjoint outputs, same inputs) runs concurrently on a side
     // stream, forked from and joined back into the context stream (not in timing mode, so
     // that per-kernel shares stay attributable)
-    const bool side = DIM == 3 && !c->timing && c->side_stream;
+    const bool side = DIM == 3 && !c->timing && c->side_stream && !c->fp;
     if (side) {
         const int64_t nb = n_boundary_points<DIM>(c->g);
         cudaEventRecord(c->ev_fork, c->stream);
@@ -326,6 +328,11 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
     }
     if (side) {
         cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+    } else if (DIM == 3 && BC == BC_MSD && A.fp) {
+        // F(b') was stored by the interior kernel: a light pass after it
+        const int64_t nb = n_boundary_points<DIM>(c->g);
+        LaunchTimer lt(c, KK_BOUNDARY, nb);
+        stage_boundary_msd_fb<T, STAGE><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
     } else {
         const int64_t nb = n_boundary_points<DIM>(c->g);
         LaunchTimer lt(c, KK_BOUNDARY, nb);
@@ -360,6 +367,9 @@ void enqueue_stage_t(nlse_ctx *c, int stage, double k, int step) {
     A.step = step;
     peer_ptrs<T>(c, obuf_of_stage(stage), A.peer_lo, A.peer_hi);
     A.wsend = halo_w(c);
+    A.fz = (C *)c->fz;
+    A.fp = (C *)c->fp;
+    A.per2 = c->per2;
     // (RK4_GPU) P:495-519: stages {1-3}, {4-6}, {7-9}, {10-11}
     switch (stage) {
         case 1: launch_stage<T, DIM, ORDER, BC, 1>(c, A); break;
@@ -680,6 +690,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     if (bc != NLSE_BC_DIRICHLET && bc != NLSE_BC_MSD && bc != NLSE_BC_L0) return fail(nullptr, NLSE_ERR_ARG, "unknown bc");
     if (order != NLSE_CD2 && order != NLSE_2SHOC4) return fail(nullptr, NLSE_ERR_ARG, "unknown order");
     if (prec != NLSE_FP32 && prec != NLSE_FP64) return fail(nullptr, NLSE_ERR_ARG, "unknown precision");
+    if (dims[0] * dims[1] >= (int64_t(1) << 31) || dims[2] >= (int64_t(1) << 31))
+        return fail(nullptr, NLSE_ERR_ARG, "an xy plane must have fewer than 2^31 points (32-bit in-plane indexing)");
     const int w = order == NLSE_2SHOC4 ? 2 : 1;
     int64_t z0 = 0, nloc = dims[2];
     if (dist) {
@@ -788,6 +800,13 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         // TMA needs 16-byte row strides (complex rows: nx even for fp32; V rows: nx*sizeof(T) % 16)
         if (!ok) c->interior_kind = KK_STREAM3D;
         c->tma = ok;
+        if (ok && bc == NLSE_BC_MSD && c->g.nx >= 5 && c->g.ny >= 5) {
+            c->per2 = int(2 * (c->g.nx - 2) + 2 * (c->g.ny - 4));
+            const size_t fzb = size_t(2) * size_t(c->g.sz) * cb, fpb = size_t(c->g.nz) * size_t(c->per2) * cb;
+            CREATE_TRY(cudaMalloc(&c->fz, fzb));
+            CREATE_TRY(cudaMalloc(&c->fp, fpb));
+            c->device_bytes += int64_t(fzb + fpb);
+        }
     }
 #undef CREATE_TRY
     c->persist1d = use_persist1d(c);
@@ -844,7 +863,7 @@ void nlse_destroy(nlse_ctx *c) {
     for (auto e : c->event_pool) cudaEventDestroy(e);
     for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     for (int b = 0; b < 3; b++) cudaFree(c->alloc[b]);
-    cudaFree(c->K); cudaFree(c->V); cudaFree(c->comm);
+    cudaFree(c->K); cudaFree(c->V); cudaFree(c->comm); cudaFree(c->fz); cudaFree(c->fp);
     drop_graph(c);
     cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result);
     if (c->h_div) cudaFreeHost(c->h_div);

@@ -195,8 +195,8 @@ struct HotC {
 
 // F (fsplit) P:424-428 and the RK4 stage combine (RK4_GPU) P:495-519 at one point.
 template <typename T, int STAGE>
-__device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &hc, int64_t q, int z, cplx<T> yc,
-                                          cplx<T> L, cplx<T> psi, cplx<T> kt, T v) {
+__device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &hc, int64_t q, int z, int gx, int gy,
+                                          cplx<T> yc, cplx<T> L, cplx<T> psi, cplx<T> kt, T v) {
     using C = cplx<T>;
     const T rho = (yc.x * yc.x) + (yc.y * yc.y);
     const T sr = hc.s * rho;
@@ -204,6 +204,13 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &
     T fi = tfma(hc.a, L.x, sr * yc.x);
     if (A.V) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
     C F; F.x = fr; F.y = fi;
+    if (A.fp) {
+        const int nx = int(A.g.nx), ny = int(A.g.ny), nz = int(A.g.nz);
+        if (A.g.zf_lo && z == 1) A.fz[gy * nx + gx] = F;
+        if (A.g.zf_hi && z == nz - 2) A.fz[int64_t(nx) * ny + gy * nx + gx] = F;
+        if (gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2)
+            A.fp[int64_t(z) * A.per2 + shell_u(gx, gy, nx, ny)] = F;
+    }
     if (STAGE == 1) {
         A.K[q] = F;
         store_out(A, q, z, cfma(hc.kc, F, yc));
@@ -327,7 +334,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
                 acc = cadd(acc, csub(cadd(Y0[-PX], Y0[PX]), y2));
                 acc = cadd(acc, csub(cadd(ym, yp), y2));
                 const C L = cscale(hc.ih2, acc);
-                t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, yc, L, psi, kt, v);
+                t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, gx, gy, yc, L, psi, kt, v);
             }
             ym = yc; yc = yp;
             sm1 = s0; s0 = s1;
@@ -451,7 +458,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             const C sd = cadd(cadd(cadd(Dz[-1], Dz[1]), cadd(Dz[-DPX], Dz[DPX])), cadd(dq[I0], dn));
             const C td = cfma(T(-10), dq[I1], sd);
             const C L = cfma(hc.c16h2, E, cneg(cscale(hc.c112, td)));
-            t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, yq[I0], L, psi, kt, v);
+            t3_finish<T, STAGE>(A, hc, int64_t(z) * g.sz + qrow, z, gx, gy, yq[I0], L, psi, kt, v);
         }
         // queue update (the slots of plane z-1 become those of plane z+2) and ring rotation
         dq[I2] = dn; pxq[I2] = px1; pyq[I2] = py1; yq[I2] = yz2;
