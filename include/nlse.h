@@ -149,6 +149,15 @@ nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n);
 nlse_status nlse_step_group(nlse_ctx *const *ctxs, int n, double k, int64_t nsteps);
 nlse_status nlse_diagnostics_group(nlse_ctx *const *ctxs, int n, double *mass, double *hamiltonian);
 
+/* The paper's frames model: nframes chunks of `chunk` RK4 steps; after
+ * each chunk Psi (widened to double) is written to frames + f * 2*prod(dims) (caller-owned
+ * host buffer of nframes * 2*prod(dims) doubles; pinned memory gives full PCIe speed).  The
+ * download of frame f runs on a copy stream from a device snapshot (two, double-buffered)
+ * and overlaps the compute of chunk f+1.  Frames are bitwise what nlse_step(k, chunk) +
+ * nlse_get_psi would return.  Errors as nlse_step; NLSE_ERR_OOM if the two snapshots
+ * (2 x 16 bytes per point) do not fit.  Slab mode: collective, frames of the local slab. */
+nlse_status nlse_run_frames(nlse_ctx *ctx, double k, int64_t chunk, int nframes, double *frames);
+
 /* Mass M = h^d sum |Psi|^2 and Hamiltonian
  *   H = h^d sum_p [ a sum_axes |Psi_{p+e} - Psi_p|^2 / h^2 + V_p |Psi_p|^2 - (s/2) |Psi_p|^4 ]
  * (forward differences over pairs inside the grid; reading R-DIAG;

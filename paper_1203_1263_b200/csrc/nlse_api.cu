@@ -89,6 +89,9 @@ struct nlse_ctx {
     cudaStream_t stream = nullptr;
     std::shared_ptr<StreamHolder> stream_ref;   // virtual ranks of one group share one stream
     cudaStream_t side_stream = nullptr;          // 3D boundary kernel, forked / joined per stage
+    cudaStream_t io_stream = nullptr;            // nlse_run_frames downloads
+    void *snap[2] = {nullptr, nullptr};          // nlse_run_frames: double2 snapshots of Psi
+    cudaEvent_t ev_snap[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int device = 0;
     int64_t steps_done = 0;
@@ -815,6 +818,31 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     return NLSE_OK;
 }
 
+// nsteps RK4 steps on the context stream: the persistent 1D kernel, or replays of the CUDA
+// graph of GRAPH_STEPS steps plus direct launches for the remainder.
+nlse_status enqueue_steps(nlse_ctx *c, double k, int64_t nsteps) {
+    if (c->persist1d) {
+        dispatch(c, [&](auto T, auto DIM, auto ORD, auto BCK) {
+            if constexpr (decltype(DIM)::value == 1)
+                launch_persist1d<decltype(T), decltype(ORD)::value, decltype(BCK)::value>(c, k, nsteps);
+            return 0;
+        });
+        enqueue_add_steps(c, nsteps);
+        return NLSE_OK;
+    }
+    int64_t done = 0;
+    if (graphs_enabled(c, nsteps) && ensure_graph(c, k)) {
+        for (; done + GRAPH_STEPS <= nsteps; done += GRAPH_STEPS)
+            CUDA_TRY(c, cudaGraphLaunch(c->graph_exec, c->stream));
+    }
+    if (done < nsteps) {
+        for (int64_t n = 0; n < nsteps - done; n++)
+            for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+        enqueue_add_steps(c, nsteps - done);
+    }
+    return NLSE_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -869,6 +897,12 @@ void nlse_destroy(nlse_ctx *c) {
     if (c->h_div) cudaFreeHost(c->h_div);
     if (c->h_result) cudaFreeHost(c->h_result);
     if (c->side_stream) { cudaStreamSynchronize(c->side_stream); cudaStreamDestroy(c->side_stream); }
+    if (c->io_stream) { cudaStreamSynchronize(c->io_stream); cudaStreamDestroy(c->io_stream); }
+    for (int b = 0; b < 2; b++) {
+        cudaFree(c->snap[b]);
+        if (c->ev_snap[b]) cudaEventDestroy(c->ev_snap[b]);
+        if (c->ev_copied[b]) cudaEventDestroy(c->ev_copied[b]);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     c->stream_ref.reset();    // destroys the stream with its last user
@@ -1008,26 +1042,49 @@ nlse_status nlse_step(nlse_ctx *c, double k, int64_t nsteps) {
     if ((st = check_step_args(c, k, nsteps))) return st;
     if (nsteps == 0) return NLSE_OK;
     if ((st = enqueue_halo_refresh(c))) return st;
-    if (c->persist1d) {
-        dispatch(c, [&](auto T, auto DIM, auto ORD, auto BCK) {
-            if constexpr (decltype(DIM)::value == 1)
-                launch_persist1d<decltype(T), decltype(ORD)::value, decltype(BCK)::value>(c, k, nsteps);
-            return 0;
-        });
-        enqueue_add_steps(c, nsteps);
-        return finish_steps(c, nsteps);
-    }
-    int64_t done = 0;
-    if (graphs_enabled(c, nsteps) && ensure_graph(c, k)) {
-        for (; done + GRAPH_STEPS <= nsteps; done += GRAPH_STEPS)
-            CUDA_TRY(c, cudaGraphLaunch(c->graph_exec, c->stream));
-    }
-    if (done < nsteps) {
-        for (int64_t n = 0; n < nsteps - done; n++)
-            for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
-        enqueue_add_steps(c, nsteps - done);
-    }
+    if ((st = enqueue_steps(c, k, nsteps))) return st;
     return finish_steps(c, nsteps);
+}
+
+nlse_status nlse_run_frames(nlse_ctx *c, double k, int64_t chunk, int nframes, double *frames) {
+    nlse_status st = check_ctx(c);
+    if (st) return st;
+    if (c->virtual_group) return fail(c, NLSE_ERR_ARG, "virtual ranks: nlse_run_frames is per process");
+    if (chunk < 1 || nframes < 1 || !frames) return fail(c, NLSE_ERR_ARG, "chunk >= 1, nframes >= 1 and frames != NULL");
+    if ((st = check_step_args(c, k, chunk))) return st;
+    const size_t n = size_t(c->g.n), fb = n * sizeof(double2);
+    if (!c->io_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+        if (!c->snap[b]) {
+            CUDA_TRY(c, cudaMalloc(&c->snap[b], fb));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_snap[b], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+            c->device_bytes += int64_t(fb);
+        }
+    }
+    if ((st = enqueue_halo_refresh(c))) return st;
+    for (int f = 0; f < nframes; f++) {
+        if ((st = enqueue_steps(c, k, chunk))) return st;
+        const int b = f & 1;
+        // snapshot b is free once the download of frame f-2 has finished
+        if (f >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+        double2 *snap = (double2 *)c->snap[b];
+        if (c->prec == NLSE_FP64) {
+            CUDA_TRY(c, cudaMemcpyAsync(snap, c->buf[BUF_PSI], fb, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            widen_psi<float><<<blocks_for(int64_t(n), 256), 256, 0, c->stream>>>((const float2 *)c->buf[BUF_PSI],
+                                                                                snap, int64_t(n));
+            CUDA_TRY(c, cudaGetLastError());
+        }
+        CUDA_TRY(c, cudaEventRecord(c->ev_snap[b], c->stream));
+        // the download overlaps the next chunk's compute
+        CUDA_TRY(c, cudaStreamWaitEvent(c->io_stream, c->ev_snap[b], 0));
+        CUDA_TRY(c, cudaMemcpyAsync(frames + 2 * n * size_t(f), snap, fb, cudaMemcpyDeviceToHost, c->io_stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev_copied[b], c->io_stream));
+    }
+    st = finish_steps(c, chunk * nframes);
+    CUDA_TRY(c, cudaStreamSynchronize(c->io_stream));
+    return st;
 }
 
 nlse_status nlse_step_group(nlse_ctx *const *ctxs, int n, double k, int64_t nsteps) {

@@ -90,12 +90,13 @@ def _load():
     lib.nlse_dist_connect.argtypes = [P, ctypes.c_char_p]
     lib.nlse_dist_connect_local.argtypes = [ctypes.POINTER(P), ctypes.c_int]
     lib.nlse_step_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_double, ctypes.c_int64]
+    lib.nlse_run_frames.argtypes = [P, ctypes.c_double, ctypes.c_int64, ctypes.c_int, D]
     lib.nlse_diagnostics_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, D, D]
     for f in ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device", "nlse_get_psi_device",
               "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_get_stream", "nlse_set_timing",
               "nlse_get_timing", "nlse_reset_timing", "nlse_get_info", "nlse_slab_range", "nlse_create_dist",
               "nlse_dist_export", "nlse_dist_connect", "nlse_dist_connect_local", "nlse_step_group",
-              "nlse_diagnostics_group"):
+              "nlse_diagnostics_group", "nlse_run_frames"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -107,7 +108,7 @@ EXPORTS = ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device",
            "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_last_error", "nlse_status_string",
            "nlse_destroy", "nlse_get_stream", "nlse_set_timing", "nlse_get_timing", "nlse_reset_timing",
            "nlse_get_info", "nlse_slab_range", "nlse_create_dist", "nlse_dist_export", "nlse_dist_connect",
-           "nlse_dist_connect_local", "nlse_step_group", "nlse_diagnostics_group")
+           "nlse_dist_connect_local", "nlse_step_group", "nlse_diagnostics_group", "nlse_run_frames")
 
 
 def _check(st, ctx=None):
@@ -199,6 +200,15 @@ class Solver:
 
     def nlse_step(self, k: float, nsteps: int):
         _check(lib.nlse_step(self.ctx, float(k), int(nsteps)), self.ctx)
+
+    def nlse_run_frames(self, k: float, chunk: int, nframes: int, out=None):
+        """nframes x (chunk RK4 steps, then Psi to frame f); returns complex128 (nframes, *shape)."""
+        if out is None:
+            out = np.empty((int(nframes),) + self.shape, dtype=np.complex128)
+        assert out.dtype == np.complex128 and out.flags.c_contiguous and out.shape == (int(nframes),) + self.shape
+        _check(lib.nlse_run_frames(self.ctx, float(k), int(chunk), int(nframes),
+                                   out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), self.ctx)
+        return out
 
     def nlse_diagnostics(self):
         m, h = ctypes.c_double(), ctypes.c_double()

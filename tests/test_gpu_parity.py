@@ -266,3 +266,23 @@ def test_config5_gpe3d_full_size_sampled():
         r = np.ascontiguousarray(ref[keep].astype(np.complex128))
         assert g.size > 0
         assert np.array_equal(g.view(np.uint64), r.view(np.uint64)), (cz, cy, cx, rel_l2(g, r))
+
+
+@pytest.mark.parametrize("ndim,precision,chunk", [(3, "fp64", 20), (3, "fp32", 3), (1, "fp64", 7), (2, "fp64", 5)])
+def test_run_frames_equal_step_then_get(ndim, precision, chunk):
+    """nlse_run_frames (the paper's frames model, downloads overlapped with compute) returns
+    exactly what nlse_step(k, chunk) + nlse_get_psi give, frame by frame."""
+    from paper_1203_1263_b200.nlse import Solver
+    dims = {1: (301,), 2: (70, 41), 3: (40, 26, 22)}[ndim]
+    h = {1: 0.1, 2: 0.2, 3: 0.5}[ndim]
+    psi0 = case_input(dims, seed=81)
+    k = _k(ndim, h, "2shoc")
+    kw = dict(s=-1.0, bc="msd", scheme="2shoc", precision=precision, force_dt=True)
+    with Solver(dims, h, **kw) as sv:
+        sv.nlse_set_psi(psi0)
+        frames = sv.nlse_run_frames(k, chunk, 3)
+    with Solver(dims, h, **kw) as sv:
+        sv.nlse_set_psi(psi0)
+        for f in range(3):
+            sv.nlse_step(k, chunk)
+            assert np.array_equal(frames[f].view(np.uint64), sv.nlse_get_psi().view(np.uint64)), f
