@@ -92,6 +92,8 @@ template <typename T> struct StageArgs {
     // (nz x per2, indexed by shell_u).  nullptr: the boundary kernel recomputes F(b').
     cplx<T> *fz, *fp;
     int per2;
+    int stream_hints;     // 1: L2 evict-first hints on the once-per-stage streams (measured slower, off)
+    int ring_rot;         // 1: rotate the 3D ring-D duty over the warps plane by plane
 };
 
 // Index of an in-plane point one step in from the x/y faces (nx, ny >= 5), in the order:

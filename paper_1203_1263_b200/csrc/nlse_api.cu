@@ -370,6 +370,20 @@ void enqueue_stage_t(nlse_ctx *c, int stage, double k, int step) {
     A.step = step;
     peer_ptrs<T>(c, obuf_of_stage(stage), A.peer_lo, A.peer_hi);
     A.wsend = halo_w(c);
+    {
+        static const int env_hints = [] {
+            const char *e = getenv("NLSE_L2_HINTS");
+            return e ? std::atoi(e) : -1;
+        }();
+        const int64_t state_bytes = c->g.n * int64_t(4 * 2 * c->eb + (c->hasV ? c->eb : 0));
+        A.stream_hints = env_hints >= 0 ? env_hints : 0;   // r01y: evict-first hints were slower
+        (void)state_bytes;
+        static const int env_rot = [] {
+            const char *e = getenv("NLSE_RING_ROT");
+            return e ? std::atoi(e) : 1;
+        }();
+        A.ring_rot = env_rot;
+    }
     A.fz = (C *)c->fz;
     A.fp = (C *)c->fp;
     A.per2 = c->per2;

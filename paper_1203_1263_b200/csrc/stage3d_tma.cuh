@@ -55,6 +55,21 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+// TMA load with an L2 cache policy (createpolicy): used with evict_first for the streams
+// read once per stage (Psi, K_tot, V) so that they do not push out the Y halo lines the
+// neighbouring tiles re-read
+__device__ __forceinline__ void tma_load_3d_hint(unsigned dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                                 unsigned bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void mbar_inval(unsigned bar) {
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
@@ -211,15 +226,17 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &
         if (gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2)
             A.fp[int64_t(z) * A.per2 + shell_u(gx, gy, nx, ny)] = F;
     }
+    // K_tot is re-read only by the next stage: a streaming store when the grid exceeds L2
+    auto store_k = [&](C kv) { if (A.stream_hints) __stcs(A.K + q, kv); else A.K[q] = kv; };
     if (STAGE == 1) {
-        A.K[q] = F;
+        store_k(F);
         store_out(A, q, z, cfma(hc.kc, F, yc));
     } else if (STAGE == 4) {
         const C r4 = cfma(hc.kc, cadd(kt, F), psi);
         store_out(A, q, z, r4);
         if (!(isfinite(r4.x) && isfinite(r4.y))) atomicMin(A.diverged, *A.step_base + A.step);
     } else {
-        A.K[q] = cfma(T(2), F, kt);
+        store_k(cfma(T(2), F, kt));
         store_out(A, q, z, cfma(hc.kc, F, psi));
     }
 }
@@ -260,6 +277,15 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         const unsigned bar = bar0 + 8 * (NS + s);
         unsigned char *dst = sm + Cfg::OFF_PKV + s * Cfg::PKVSLOT;
         mbar_expect_tx(bar, pkv_bytes);
+        if (A.stream_hints) {
+            const uint64_t pol = policy_evict_first();
+            if (STAGE != 1) {
+                tma_load_3d_hint(smem_u32(dst), mP, 2 * x0, y0, p + g.zghost, bar, pol);
+                tma_load_3d_hint(smem_u32(dst + Cfg::OWN_C), mK, 2 * x0, y0, p, bar, pol);
+            }
+            if (A.V) tma_load_3d_hint(smem_u32(dst + 2 * Cfg::OWN_C), mV, x0, y0, p, bar, pol);
+            return;
+        }
         if (STAGE != 1) {
             tma_load_3d(smem_u32(dst), mP, 2 * x0, y0, p + g.zghost, bar);
             tma_load_3d(smem_u32(dst + Cfg::OWN_C), mK, 2 * x0, y0, p, bar);
@@ -289,15 +315,20 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     const int downo = ty * DPX + tx;                   // ... in a D tile
     const int pown = ty * TX + tx;                     // ... in an owned-box (Psi/K/V) tile
     const int64_t qrow = int64_t(gy) * g.sy + gx;     // global offset in plane 0
-    // ring assignment (2SHOC): warp 0 row -1, warp 1 row TY, warp 2 columns -1 and TX
+    // ring duty (2SHOC): role 0 = row -1, role 1 = row TY, role 2 = columns -1 and TX; in
+    // iteration j the roles go to warps j, j+1, j+2 (mod TY), so the extra D evaluations
+    // rotate over all warps instead of always slowing the same three
+    auto ring_pos = [&](int jj, int &rx, int &ry) -> bool {
+        const int role = A.ring_rot ? (ty + Cfg::TY - (jj % Cfg::TY)) % Cfg::TY : ty;
+        if (role == 0) { rx = tx; ry = -1; return true; }
+        if (role == 1) { rx = tx; ry = Cfg::TY; return true; }
+        if (role == 2 && tx < 2 * Cfg::TY) { rx = tx < Cfg::TY ? -1 : TX; ry = tx % Cfg::TY; return true; }
+        rx = 0; ry = 0;
+        return false;
+    };
     int rlx = 0, rly = 0;
-    bool ring = false;
-    if (ORDER == ORDER_2SHOC) {
-        if (ty == 0) { ring = true; rlx = tx; rly = -1; }
-        else if (ty == 1) { ring = true; rlx = tx; rly = Cfg::TY; }
-        else if (ty == 2 && tx < 2 * Cfg::TY) { ring = true; rlx = tx < Cfg::TY ? -1 : TX; rly = tx % Cfg::TY; }
-    }
-    const int ro = rly * PX + rlx, rdo = rly * DPX + rlx;
+    bool ring = ORDER == ORDER_2SHOC && ring_pos(0, rlx, rly);
+    int ro = rly * PX + rlx, rdo = rly * DPX + rlx;
 
     // PKV ring position of plane z
     int ps = 0; unsigned pp = 0;
@@ -425,6 +456,9 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             dn = cscale(hc.ih2, acc);
         }
         b.dslot(d1s)[downo] = dn;
+        ring = ring_pos(j + 1, rlx, rly);
+        ro = rly * PX + rlx;
+        rdo = rly * DPX + rlx;
         if (ring) {
             C dr;
             if (EDGE) {
