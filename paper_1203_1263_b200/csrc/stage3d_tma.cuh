@@ -348,7 +348,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         // slots of planes z-1, z, z+1 (relative index p - zbase: 0, 1, 2 at z = zs)
         int sm1 = 0, s0 = 1, s1 = 2;
         unsigned par1 = 0;                            // parity of plane z+1's slot use
-        if (zs - 1 >= zl_lo) mbar_wait(bar0 + 8 * sm1, 0);
+        mbar_wait(bar0 + 8 * sm1, 0);                // (arrive-only when below a z face)
         mbar_wait(bar0 + 8 * s0, 0);
         C ym = b.yslot(sm1)[own], yc = b.yslot(s0)[own];
         for (int z = zs; z < ze; z++) {
@@ -390,7 +390,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     // queue rotation is pure register renaming.
     int sm1 = 1, s0 = 2, s1 = 3, s2 = 4;              // Y slots of planes z-1 .. z+2 at z = zs
     unsigned par2 = 0;                                // parity of plane z+2's slot use
-    if (zs - 2 >= zl_lo) mbar_wait(bar0 + 0, 0);
+    mbar_wait(bar0 + 0, 0);                           // (arrive-only when below a z face)
     mbar_wait(bar0 + 8 * sm1, 0);
     mbar_wait(bar0 + 8 * s0, 0);
     mbar_wait(bar0 + 8 * s1, 0);
@@ -459,6 +459,9 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         ring = ring_pos(j + 1, rlx, rly);
         ro = rly * PX + rlx;
         rdo = rly * DPX + rlx;
+        // on the upper z face the ring D(z+1) needs D(z) at the same ring point, written in the
+        // previous iteration by the warp that had this ring role then: wait for phase j first
+        if (ring && zf1) mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
         if (ring) {
             C dr;
             if (EDGE) {
@@ -483,7 +486,11 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
         const C eyz = csub(cadd(pyq[I0], py1), y4);
         const C E = cadd(cadd(exy, exz), eyz);
         mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
-        if (issuer) { issue_y(z + H + P); issue_pkv(z + Cfg::PP); }
+        // the issuer rotates with the plane too (a warp without ring duty this plane)
+        if (tx == 0 && ty == (A.ring_rot ? (j + 3) % Cfg::TY : Cfg::TY - 1)) {
+            issue_y(z + H + P);
+            issue_pkv(z + Cfg::PP);
+        }
         C psi, kt; T v;
         pkv_wait();
         load_own(psi, kt, v);
