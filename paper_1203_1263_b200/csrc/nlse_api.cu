@@ -39,7 +39,10 @@ static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
 
 struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
 
-constexpr int TMA_P = 3;        // TMA ring prefetch depth of the Y planes (planes ahead)
+#ifndef NLSE_TMA_P
+#define NLSE_TMA_P 3
+#endif
+constexpr int TMA_P = NLSE_TMA_P;  // TMA ring prefetch depth of the Y planes (planes ahead; 2 and 4 measured slower, r01 ab1)
 constexpr int GRAPH_STEPS = 8;  // RK4 steps per captured CUDA graph
 
 enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2 };

@@ -95,7 +95,12 @@ struct T3Cfg {
     // Psi/K/V prefetch depth (planes ahead); Y uses P.  A slot is refilled only once every
     // thread has finished the plane two planes back (see the barrier protocol in t3_run),
     // hence ring sizes P + 4 (Y: the planes in use reach two ahead) and PP + 2.
-    static constexpr int PP = (sizeof(T) == 8) ? 2 : 3;
+    // PP = 3 for fp64 measured 1.5 % faster than 2 (r01 ab1: 68.7 vs 69.8 ms/step at 1024^3,
+    // 222 KB of shared memory per CTA at TY = 16); NLSE_TMA_PP64 overrides (A/B builds)
+#ifndef NLSE_TMA_PP64
+#define NLSE_TMA_PP64 3
+#endif
+    static constexpr int PP = (sizeof(T) == 8) ? NLSE_TMA_PP64 : 3;
     static constexpr int NS = P + 4, NP = PP + 2, ND = (ORDER == ORDER_2SHOC) ? 4 : 0;
     static constexpr int DPX = TX + 2, DPY = TY + 2;
     static constexpr int up128(int b) { return (b + 127) / 128 * 128; }

@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnlse_b200.so")
+# NLSE_LIB selects a variant build of the same library (scripts/build_variant.py, A/B
+# measurements only); the default is the in-tree libnlse_b200.so
+LIB_PATH = os.environ.get("NLSE_LIB") or os.path.join(_HERE, "libnlse_b200.so")
 
 NLSE_OK, NLSE_ERR_ARG, NLSE_ERR_UNSTABLE, NLSE_ERR_OOM, NLSE_ERR_CUDA, NLSE_ERR_COMM, NLSE_ERR_DIVERGED = range(7)
 NLSE_BC_DIRICHLET, NLSE_BC_MSD, NLSE_BC_L0 = 0, 1, 2
