@@ -524,6 +524,329 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
     if (z < ze) body(std::integral_constant<int, 1>(), z++);
 }
 
+// Shared-memory access by 32-bit shared-window address (the fast path keeps one base
+// register instead of re-deriving the window base of the dynamic shared memory per access).
+__device__ __forceinline__ double2 lds_c(unsigned a, double) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_c(unsigned a, float) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_r(unsigned a, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_r(unsigned a, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_c(unsigned a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts_c(unsigned a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+// a value the compiler must keep (it cannot re-derive it from the shared-window base)
+__device__ __forceinline__ unsigned opaque_u32(unsigned x) {
+    unsigned r;
+    asm volatile("mov.u32 %0, %1;\n" : "=r"(r) : "r"(x));
+    return r;
+}
+
+// v2.3: the 2SHOC loop of t3_run for interior tiles (EDGE = false) with the per-plane
+// control work cut down (ncu source counters, r01 ncus: the v2.2 loop issued ~275 warp
+// instructions per point-stage, ~85 of them fp64): shared memory by 32-bit addresses from
+// one base register, ring offsets by arithmetic on the role, output / K_tot pointers
+// advanced by one plane stride, the rare per-plane cases (F at the b' planes, neighbour
+// stores) behind one uniform test each, and the one iteration that can meet the upper z
+// face peeled out of the unrolled loop.  Same rings, barrier protocol and per-point DAG as
+// t3_run, so the same bits.
+template <typename T, int BC, int STAGE, int P, int TYV>
+__device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap *mP, const CUtensorMap *mK,
+                                        const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
+                                        int y0, int zs, int ze) {
+    using C = cplx<T>;
+    using Cfg = T3Cfg<T, ORDER_2SHOC, P, TYV>;
+    using B = T3Body<T, ORDER_2SHOC, BC, STAGE, P, TYV, false>;
+    constexpr int H = Cfg::H, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
+    constexpr int CB = Cfg::CB;
+    constexpr unsigned YS = Cfg::YSLOT, DS = Cfg::DSLOT, PS = Cfg::PKVSLOT;
+    static_assert((TY & (TY - 1)) == 0 && TY >= 4, "ring roles by mask need a power-of-two TY");
+    const B b{A, sm, x0, y0};
+    const HotC<T> hc(A.c);
+    const Grid &g = A.g;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int nz = int(g.nz);
+    const int zmem_lo = g.zf_lo ? 0 : -g.zghost, zmem_hi = nz + (g.zf_hi ? 0 : g.zghost);
+    const int zl_lo = max(zs - H, zmem_lo), zl_hi = min(ze + H - 1, zmem_hi - 1);
+    const int zbase = zs - H;
+    const unsigned sb = opaque_u32(smem_u32(sm));
+    const unsigned bar0 = sb + Cfg::OFF_BAR;
+    const bool hasV = A.V != nullptr;
+    const unsigned pkv_bytes = (STAGE != 1 ? 2u * Cfg::OWN_C : 0u) + (hasV ? unsigned(Cfg::OWN_R) : 0u);
+
+    auto issue_y = [&](int p) {
+        if (p > zl_hi) return;
+        const int s = (p - zbase) % NS;
+        const unsigned bar = bar0 + 8 * s;
+        if (p < zl_lo) { mbar_arrive(bar); return; }
+        mbar_expect_tx(bar, Cfg::YBYTES);
+        tma_load_3d(sb + s * YS, mY, 2 * (x0 - Cfg::HX), y0 - H, p + g.zghost, bar);
+    };
+    auto issue_pkv = [&](int p) {
+        if (p >= ze || pkv_bytes == 0) return;
+        const int s = (p - zs) % NP;
+        const unsigned bar = bar0 + 8 * (NS + s);
+        const unsigned dst = sb + Cfg::OFF_PKV + s * PS;
+        mbar_expect_tx(bar, pkv_bytes);
+        if (STAGE != 1) {
+            tma_load_3d(dst, mP, 2 * x0, y0, p + g.zghost, bar);
+            tma_load_3d(dst + Cfg::OWN_C, mK, 2 * x0, y0, p, bar);
+        }
+        if (hasV) tma_load_3d(dst + 2 * Cfg::OWN_C, mV, x0, y0, p, bar);
+    };
+    const unsigned cbar0 = bar0 + 8 * (NS + NP);
+    if (tid == 0) {
+        for (int i = 0; i < NS + NP; i++) mbar_init(bar0 + 8 * i, 1);
+        mbar_init(cbar0, Cfg::NT);
+        mbar_init(cbar0 + 8, Cfg::NT);
+        fence_proxy_async();
+    }
+    __syncthreads();
+    if (tid == Cfg::NT - 32) {
+        for (int p = zbase; p <= zs + H + P - 1; p++) issue_y(p);
+        for (int p = zs; p <= zs + Cfg::PP - 1; p++) issue_pkv(p);
+    }
+
+    const int gx = x0 + tx, gy = y0 + ty;
+    const int nx = int(g.nx);
+    // shared addresses of this thread's point in Y slot 0, D slot 0 and Psi/K/V slot 0
+    const unsigned ownY = sb + unsigned(((ty + H) * PX + tx + Cfg::HX) * CB);
+    const unsigned ownD = sb + unsigned(Cfg::OFF_D + ((ty + 1) * DPX + tx + 1) * CB);
+    const unsigned ownP = sb + unsigned(Cfg::OFF_PKV + (ty * TX + tx) * CB);
+    const unsigned ownV = sb + unsigned(Cfg::OFF_PKV + 2 * Cfg::OWN_C + (ty * TX + tx) * int(sizeof(T)));
+    auto ldY = [&](unsigned slotB, int d) -> C { return lds_c(ownY + slotB + unsigned(d * CB), T()); };
+    // ring duty: role 0 = row -1, 1 = row TY, 2 = columns -1 and TX (2 TY lanes), 3 = none;
+    // role of warp ty in iteration jj = (ty - jj) mod TY with rotation, ty without
+    const bool rot = A.ring_rot != 0;
+    auto ring_role = [&](int jj) {
+        const int r = rot ? ((ty - jj) & (TY - 1)) : ty;
+        return (r > 2 || (r == 2 && tx >= 2 * TY)) ? 3 : r;
+    };
+    // (lx, ly) of a role's ring point -> offsets inside a Y slot / a D slot (bytes)
+    auto ring_xy = [&](int role, int &rx, int &ry) {
+        rx = role == 2 ? (tx < TY ? -1 : TX) : tx;
+        ry = role == 0 ? -1 : (role == 1 ? TY : (tx & (TY - 1)));
+    };
+    // global pointers of the owned point at plane zs, advanced by one plane per iteration
+    const int64_t sz = g.sz;
+    const int64_t qrow = int64_t(gy) * g.sy + gx;
+    C *outp = A.out + (int64_t(zs) * sz + qrow);
+    C *kp = A.K + (int64_t(zs) * sz + qrow);
+    const int zf1_at = g.zf_hi ? nz - 2 : INT32_MIN;              // z + 1 is the upper z face
+    const bool fpz = A.fp != nullptr;
+    const int fz_lo = (fpz && g.zf_lo) ? 1 : INT32_MIN, fz_hi = (fpz && g.zf_hi) ? nz - 2 : INT32_MIN;
+    const bool peers = A.peer_lo != nullptr || A.peer_hi != nullptr;
+
+    // ---------------------------------------------------------------- prologue (t3_run)
+    int s2 = 4;
+    unsigned par2 = 0;
+    unsigned yB0 = 2 * YS, yB1 = 3 * YS, yB2 = 4 * YS;          // Y slots of planes z, z+1, z+2
+    mbar_wait(bar0 + 0, 0);
+    mbar_wait(bar0 + 8 * 1, 0);
+    mbar_wait(bar0 + 8 * 2, 0);
+    mbar_wait(bar0 + 8 * 3, 0);
+    unsigned dB0 = 0;                                   // D slot (byte offset) of plane z
+    C yq[3], dq[3], pxq[3], pyq[3];
+    {
+        const unsigned yBm = 1 * YS, yBmm = 0;
+        yq[0] = ldY(yB0, 0);
+        yq[1] = ldY(yB1, 0);
+        pxq[1] = cadd(ldY(yB0, -1), ldY(yB0, 1));
+        pyq[1] = cadd(ldY(yB0, -PX), ldY(yB0, PX));
+        pxq[0] = cadd(ldY(yBm, -1), ldY(yBm, 1));
+        pyq[0] = cadd(ldY(yBm, -PX), ldY(yBm, PX));
+        {
+            const C y2 = cadd(yq[0], yq[0]);
+            C acc = csub(pxq[1], y2);
+            acc = cadd(acc, csub(pyq[1], y2));
+            acc = cadd(acc, csub(cadd(ldY(yBm, 0), yq[1]), y2));
+            dq[1] = cscale(A.c.ih2, acc);
+        }
+        sts_c(ownD + dB0, dq[1]);
+        const int role = ring_role(0);
+        if (role < 3) {
+            int rx, ry;
+            ring_xy(role, rx, ry);
+            const int oy = ((ry - ty) * PX + (rx - tx)) * CB, od = ((ry - ty) * DPX + (rx - tx)) * CB;
+            const unsigned a0 = ownY + unsigned(oy);
+            const C yc = lds_c(a0 + yB0, T());
+            const C y2 = cadd(yc, yc);
+            C acc = csub(cadd(lds_c(a0 + yB0 - CB, T()), lds_c(a0 + yB0 + CB, T())), y2);
+            acc = cadd(acc, csub(cadd(lds_c(a0 + yB0 - PX * CB, T()), lds_c(a0 + yB0 + PX * CB, T())), y2));
+            acc = cadd(acc, csub(cadd(lds_c(a0 + yBm, T()), lds_c(a0 + yB1, T())), y2));
+            sts_c(ownD + dB0 + unsigned(od), cscale(A.c.ih2, acc));
+        }
+        const C ym = ldY(yBm, 0);
+        if (g.zf_lo && zs - 1 == 0) {
+            dq[0] = b.D_bc(qrow, ym, sz + qrow, yq[0], dq[1]);
+        } else {
+            const C y2 = cadd(ym, ym);
+            C acc = csub(pxq[0], y2);
+            acc = cadd(acc, csub(pyq[0], y2));
+            acc = cadd(acc, csub(cadd(ldY(yBmm, 0), yq[0]), y2));
+            dq[0] = cscale(A.c.ih2, acc);
+        }
+    }
+    mbar_arrive(cbar0);
+    int j = 0;
+    unsigned pB = 0, pp = 0;                            // Psi/K/V slot (byte offset) of plane z, parity
+    int ps = 0;
+
+    // one plane; ZF: this iteration may be the one whose z + 1 is the upper z face
+    auto body = [&](auto phase, auto zfc, int z) {
+        constexpr int PH = decltype(phase)::value;
+        constexpr bool ZF = decltype(zfc)::value;
+        constexpr int I0 = PH, I1 = (PH + 1) % 3, I2 = (PH + 2) % 3;
+        const bool zf1 = ZF && (z == zf1_at);
+        const unsigned dB1 = (dB0 + DS == 4 * DS) ? 0u : dB0 + DS;
+        if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
+        const C px1 = cadd(ldY(yB1, -1), ldY(yB1, 1));
+        const C py1 = cadd(ldY(yB1, -PX), ldY(yB1, PX));
+        C yz2 = yq[I1], dn;
+        if (zf1) {
+            dn = b.D_bc(int64_t(z + 1) * sz + qrow, yq[I1], int64_t(z) * sz + qrow, yq[I0], dq[I1]);
+        } else {
+            yz2 = ldY(yB2, 0);
+            const C y2 = cadd(yq[I1], yq[I1]);
+            C acc = csub(px1, y2);
+            acc = cadd(acc, csub(py1, y2));
+            acc = cadd(acc, csub(cadd(yq[I0], yz2), y2));
+            dn = cscale(hc.ih2, acc);
+        }
+        sts_c(ownD + dB1, dn);
+        const int role = ring_role(j + 1);
+        if (role < 3) {
+            int rx, ry;
+            ring_xy(role, rx, ry);
+            const int oy = ((ry - ty) * PX + (rx - tx)) * CB, od = ((ry - ty) * DPX + (rx - tx)) * CB;
+            const unsigned a0 = ownY + unsigned(oy);
+            C dr;
+            if (zf1) {
+                // D(z) at this ring point was written by the warp that had this role in the
+                // previous iteration: wait for phase j first
+                mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
+                dr = b.D_bc(b.gq(z + 1, rx, ry), lds_c(a0 + yB1, T()), b.gq(z, rx, ry), lds_c(a0 + yB0, T()),
+                            lds_c(ownD + dB0 + unsigned(od), T()));
+            } else {
+                const C yc = lds_c(a0 + yB1, T());
+                const C y2 = cadd(yc, yc);
+                C acc = csub(cadd(lds_c(a0 + yB1 - CB, T()), lds_c(a0 + yB1 + CB, T())), y2);
+                acc = cadd(acc, csub(cadd(lds_c(a0 + yB1 - PX * CB, T()), lds_c(a0 + yB1 + PX * CB, T())), y2));
+                acc = cadd(acc, csub(cadd(lds_c(a0 + yB0, T()), lds_c(a0 + yB2, T())), y2));
+                dr = cscale(hc.ih2, acc);
+            }
+            sts_c(ownD + dB1 + unsigned(od), dr);
+        }
+        mbar_arrive(cbar0 + 8 * ((j + 1) & 1));
+        const C y2c = cadd(yq[I0], yq[I0]);
+        const C y4 = cadd(y2c, y2c);
+        const C pxa = cadd(ldY(yB0, -PX - 1), ldY(yB0, -PX + 1));
+        const C pxb = cadd(ldY(yB0, PX - 1), ldY(yB0, PX + 1));
+        const C exy = csub(cadd(pxa, pxb), y4);
+        const C exz = csub(cadd(pxq[I0], px1), y4);
+        const C eyz = csub(cadd(pyq[I0], py1), y4);
+        const C E = cadd(cadd(exy, exz), eyz);
+        mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
+        if (tx == 0 && ty == (rot ? ((j + 3) & (TY - 1)) : TY - 1)) {
+            issue_y(z + H + P);
+            issue_pkv(z + Cfg::PP);
+        }
+        C psi, kt; T v;
+        if (pkv_bytes) mbar_wait(bar0 + 8 * (NS + ps), pp);
+        if (STAGE != 1) {
+            psi = lds_c(ownP + pB, T());
+            kt = lds_c(ownP + pB + Cfg::OWN_C, T());
+        }
+        if (hasV) v = lds_r(ownV + pB, T());
+        const unsigned ad = ownD + dB0;
+        const C sd = cadd(cadd(cadd(lds_c(ad - CB, T()), lds_c(ad + CB, T())),
+                               cadd(lds_c(ad - DPX * CB, T()), lds_c(ad + DPX * CB, T()))),
+                          cadd(dq[I0], dn));
+        const C td = cfma(T(-10), dq[I1], sd);
+        const C L = cfma(hc.c16h2, E, cneg(cscale(hc.c112, td)));
+        // F (fsplit) P:424-428 and the stage combine (RK4_GPU) P:495-519 (as t3_finish)
+        const C yc = yq[I0];
+        const T rho = (yc.x * yc.x) + (yc.y * yc.y);
+        const T sr = hc.s * rho;
+        T fr = tfma(-hc.a, L.y, -(sr * yc.y));
+        T fi = tfma(hc.a, L.x, sr * yc.x);
+        if (hasV) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
+        C F; F.x = fr; F.y = fi;
+        if (z == fz_lo || z == fz_hi) {
+            if (z == fz_lo) A.fz[gy * nx + gx] = F;
+            if (z == fz_hi) A.fz[int64_t(nx) * g.ny + gy * nx + gx] = F;
+        }
+        C o;
+        if (STAGE == 1) {
+            *kp = F;
+            o = cfma(hc.kc, F, yc);
+        } else if (STAGE == 4) {
+            o = cfma(hc.kc, cadd(kt, F), psi);
+        } else {
+            *kp = cfma(T(2), F, kt);
+            o = cfma(hc.kc, F, psi);
+        }
+        *outp = o;
+        if (peers) {                                    // slab mode: the neighbours' ghost planes
+            const int64_t q = outp - A.out;
+            if (A.peer_lo && z < A.wsend) A.peer_lo[q] = o;
+            if (A.peer_hi && z >= nz - A.wsend) A.peer_hi[q] = o;
+        }
+        if (STAGE == 4 && !(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
+        outp += sz;
+        kp += sz;
+        // queue update and slot rotation
+        dq[I2] = dn; pxq[I2] = px1; pyq[I2] = py1; yq[I2] = yz2;
+        yB0 = yB1; yB1 = yB2;
+        if (++s2 == NS) { s2 = 0; par2 ^= 1u; }
+        yB2 = s2 * YS;
+        dB0 = dB1;
+        if (++ps == NP) { ps = 0; pp ^= 1u; }
+        pB = ps * PS;
+        ++j;
+    };
+    using F0 = std::false_type;
+    using F1 = std::true_type;
+    using P0 = std::integral_constant<int, 0>;
+    using P1 = std::integral_constant<int, 1>;
+    using P2 = std::integral_constant<int, 2>;
+    int z = zs;
+    const int zlast = ze - 1;                           // the only iteration that can meet the upper face
+    for (; z + 3 <= zlast; z += 3) {
+        body(P0(), F0(), z);
+        body(P1(), F0(), z + 1);
+        body(P2(), F0(), z + 2);
+    }
+    const int rem = zlast - z;                          // 0, 1 or 2 iterations before zlast
+    if (rem == 0) {
+        body(P0(), F1(), z);
+    } else if (rem == 1) {
+        body(P0(), F0(), z);
+        body(P1(), F1(), z + 1);
+    } else {
+        body(P0(), F0(), z);
+        body(P1(), F0(), z + 1);
+        body(P2(), F1(), z + 2);
+    }
+}
+
 // One CTA per work item (tile, z chunk); blockIdx.x enumerates the items z-chunk-major,
 // then tile row, then tile column, so the CTAs resident at any time cover whole bands of
 // consecutive tiles of one z chunk (their shared halo rows and columns are L2 hits).
@@ -549,6 +872,7 @@ stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUte
     // every owned and ring point in-plane interior -> branch-free path
     const bool edge = force_edge || !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
     if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    else if constexpr (ORDER == ORDER_2SHOC) t3_fast<T, BC, STAGE, P, TYV>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
     else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
 }
 
