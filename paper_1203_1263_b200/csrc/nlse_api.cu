@@ -284,13 +284,13 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
     const int64_t items = int64_t(gx) * gy * gz;
-    static const bool force_edge = [] {      // debug / measurement: every tile on the face-aware path
-        const char *e = getenv("NLSE_FORCE_EDGE");
-        return e && e[0] == '1';
-    }();
+    // debug / measurement / tests: NLSE_FORCE_EDGE=1 runs every tile on the face-aware lean
+    // loop, =2 every tile on the per-point face path (t3_run, EDGE)
+    const char *fe = getenv("NLSE_FORCE_EDGE");
+    const int force_edge = (fe && (fe[0] == '1' || fe[0] == '2')) ? fe[0] - '0' : 0;
     stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
         c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
-        force_edge ? 1 : 0);
+        force_edge);
 }
 
 template <typename T, int ORDER, int BC, int STAGE>

@@ -567,7 +567,14 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
 // stores) behind one uniform test each, and the one iteration that can meet the upper z
 // face peeled out of the unrolled loop.  Same rings, barrier protocol and per-point DAG as
 // t3_run, so the same bits.
-template <typename T, int BC, int STAGE, int P, int TYV>
+// EDGE = true: a tile whose owned points touch an x/y face or leave the grid, but whose ring
+// has no face point (x0 + TX != nx - 1, y0 + TY != ny - 1; t3_lean_ok).  Every point takes the
+// stencil D; face points then replace it by the Laplacian form of the BC ((BCDlap) P:320-323,
+// (BCMSDlap) P:336-344) from Y_b, Y_b', D_b' (x faces: D_b' by a lane shuffle; y faces: the
+// stencil at b' again) and V_b, V_b' prefetched one plane ahead into registers.  Edge, corner
+// and out-of-grid points keep the stencil value, which no output reads (R-DFACE); only
+// interior points are stored.
+template <typename T, int BC, int STAGE, int P, int TYV, bool EDGE>
 __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap *mP, const CUtensorMap *mK,
                                         const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
                                         int y0, int zs, int ze) {
@@ -625,7 +632,19 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
     }
 
     const int gx = x0 + tx, gy = y0 + ty;
-    const int nx = int(g.nx);
+    const int nx = int(g.nx), ny = int(g.ny);
+    // point classes (fixed along z): ok = in-plane interior (an output point); xf / yf = on
+    // exactly one x / y face (D by the BC); everything else (edges, corners, outside) unused
+    const bool ing = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+    const bool fxp = gx == 0 || gx == nx - 1, fyp = gy == 0 || gy == ny - 1;
+    const bool ok = !EDGE || (ing && !fxp && !fyp);
+    const bool xf = EDGE && ing && fxp && !fyp, yf = EDGE && ing && fyp && !fxp;
+    const int srcl = (gx == 0) ? tx + 1 : tx - 1;        // lane of b' for an x-face point
+    const int dyb = (gy == 0) ? 1 : -1;                   // row step to b' for a y-face point
+    const int64_t qb1off = xf ? (gx == 0 ? 1 : -1) : (yf ? int64_t(dyb) * g.sy : 0);
+    // in-plane ring of points one in from the x/y faces: F(b') for the MSD boundary pass
+    const bool shell = EDGE && ok && A.fp != nullptr && (gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2);
+    const int shell_i = shell ? shell_u(gx, gy, nx, ny) : 0;
     // shared addresses of this thread's point in Y slot 0, D slot 0 and Psi/K/V slot 0
     const unsigned ownY = sb + unsigned(((ty + H) * PX + tx + Cfg::HX) * CB);
     const unsigned ownD = sb + unsigned(Cfg::OFF_D + ((ty + 1) * DPX + tx + 1) * CB);
@@ -653,6 +672,60 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
     const bool fpz = A.fp != nullptr;
     const int fz_lo = (fpz && g.zf_lo) ? 1 : INT32_MIN, fz_hi = (fpz && g.zf_hi) ? nz - 2 : INT32_MIN;
     const bool peers = A.peer_lo != nullptr || A.peer_hi != nullptr;
+    // face points: V at b and b' of a plane (global, read one plane ahead; planes outside
+    // [0, nz) have no V and their face D is never read)
+    const bool vface = (xf || yf) && hasV && BC != BC_L0;
+    auto ld_vface = [&](int p, T &vb, T &vb1) {
+        if (vface && p >= 0 && p < nz) {
+            const int64_t q = int64_t(p) * sz + qrow;
+            vb = __ldg(A.V + q);
+            vb1 = __ldg(A.V + q + qb1off);
+        }
+    };
+    // the BC form of D at a face point from Y_b, Y_b', D_b' (the same operations as
+    // T3Body::D_bc, with V passed in)
+    auto dface = [&](C yb, T vb, C y1, T vb1, C d1) -> C {
+        if (BC == BC_L0) { C zr; zr.x = T(0); zr.y = T(0); return zr; }
+        T nb = A.c.s * ((yb.x * yb.x) + (yb.y * yb.y));
+        if (hasV) nb = nb - vb;
+        if (BC == BC_DIRICHLET) {
+            const T t = A.c.inv_a * nb;
+            C r; r.x = -(t * yb.x); r.y = -(t * yb.y);
+            return r;
+        } else {
+            const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+            T re = T(0);
+            if (!(rho1 < A.c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+            T n1 = A.c.s * rho1;
+            if (hasV) n1 = n1 - vb1;
+            const T gg = re + ((n1 - nb) * A.c.inv_a);
+            return cscale(gg, yb);
+        }
+    };
+    // stencil D at the point d bytes away from the own point, planes (m, 0, p) = Y slots
+    auto dstencil = [&](unsigned yBm, unsigned yBc, unsigned yBp, int d) -> C {
+        const unsigned a0 = ownY + unsigned(d);
+        const C yc = lds_c(a0 + yBc, T());
+        const C y2 = cadd(yc, yc);
+        C acc = csub(cadd(lds_c(a0 + yBc - CB, T()), lds_c(a0 + yBc + CB, T())), y2);
+        acc = cadd(acc, csub(cadd(lds_c(a0 + yBc - PX * CB, T()), lds_c(a0 + yBc + PX * CB, T())), y2));
+        acc = cadd(acc, csub(cadd(lds_c(a0 + yBm, T()), lds_c(a0 + yBp, T())), y2));
+        return cscale(A.c.ih2, acc);
+    };
+    // replace the stencil value dst (own point, centre slot yBc) by the face BC form
+    auto face_fix = [&](C &dst, unsigned yBm, unsigned yBc, unsigned yBp, C yb, T vb, T vb1) {
+        const unsigned full = 0xffffffffu;
+        C d1x;
+        d1x.x = __shfl_sync(full, dst.x, srcl);
+        d1x.y = __shfl_sync(full, dst.y, srcl);
+        if (xf || yf) {
+            const int d = xf ? (gx == 0 ? CB : -CB) : dyb * PX * CB;
+            const C y1 = lds_c(ownY + yBc + unsigned(d), T());
+            const C d1 = xf ? d1x : dstencil(yBm, yBc, yBp, d);
+            dst = dface(yb, vb, y1, vb1, d1);
+        }
+    };
+    T vb_n = T(0), vb1_n = T(0);                        // V at b, b' of the plane z + 1
 
     // ---------------------------------------------------------------- prologue (t3_run)
     int s2 = 4;
@@ -664,6 +737,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
     mbar_wait(bar0 + 8 * 3, 0);
     unsigned dB0 = 0;                                   // D slot (byte offset) of plane z
     C yq[3], dq[3], pxq[3], pyq[3];
+    dq[0].x = T(0); dq[0].y = T(0);
     {
         const unsigned yBm = 1 * YS, yBmm = 0;
         yq[0] = ldY(yB0, 0);
@@ -678,6 +752,12 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
             acc = cadd(acc, csub(pyq[1], y2));
             acc = cadd(acc, csub(cadd(ldY(yBm, 0), yq[1]), y2));
             dq[1] = cscale(A.c.ih2, acc);
+        }
+        if (EDGE) {
+            T vb = T(0), vb1 = T(0);
+            ld_vface(zs, vb, vb1);
+            face_fix(dq[1], yBm, yB0, yB1, yq[0], vb, vb1);
+            ld_vface(zs + 1, vb_n, vb1_n);
         }
         sts_c(ownD + dB0, dq[1]);
         const int role = ring_role(0);
@@ -695,7 +775,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         }
         const C ym = ldY(yBm, 0);
         if (g.zf_lo && zs - 1 == 0) {
-            dq[0] = b.D_bc(qrow, ym, sz + qrow, yq[0], dq[1]);
+            if (ok) dq[0] = b.D_bc(qrow, ym, sz + qrow, yq[0], dq[1]);
         } else {
             const C y2 = cadd(ym, ym);
             C acc = csub(pxq[0], y2);
@@ -721,7 +801,8 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         const C py1 = cadd(ldY(yB1, -PX), ldY(yB1, PX));
         C yz2 = yq[I1], dn;
         if (zf1) {
-            dn = b.D_bc(int64_t(z + 1) * sz + qrow, yq[I1], int64_t(z) * sz + qrow, yq[I0], dq[I1]);
+            if (ok) dn = b.D_bc(int64_t(z + 1) * sz + qrow, yq[I1], int64_t(z) * sz + qrow, yq[I0], dq[I1]);
+            else dn = dq[I1];                           // edge / outside: never read
         } else {
             yz2 = ldY(yB2, 0);
             const C y2 = cadd(yq[I1], yq[I1]);
@@ -729,6 +810,10 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
             acc = cadd(acc, csub(py1, y2));
             acc = cadd(acc, csub(cadd(yq[I0], yz2), y2));
             dn = cscale(hc.ih2, acc);
+        }
+        if (EDGE && !zf1) {
+            face_fix(dn, yB0, yB1, yB2, yq[I1], vb_n, vb1_n);
+            ld_vface(z + 2, vb_n, vb1_n);
         }
         sts_c(ownD + dB1, dn);
         const int role = ring_role(j + 1);
@@ -742,8 +827,12 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
                 // D(z) at this ring point was written by the warp that had this role in the
                 // previous iteration: wait for phase j first
                 mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
-                dr = b.D_bc(b.gq(z + 1, rx, ry), lds_c(a0 + yB1, T()), b.gq(z, rx, ry), lds_c(a0 + yB0, T()),
-                            lds_c(ownD + dB0 + unsigned(od), T()));
+                const int rgx = x0 + rx, rgy = y0 + ry;
+                if (!EDGE || (rgx >= 1 && rgx <= nx - 2 && rgy >= 1 && rgy <= ny - 2))
+                    dr = b.D_bc(b.gq(z + 1, rx, ry), lds_c(a0 + yB1, T()), b.gq(z, rx, ry), lds_c(a0 + yB0, T()),
+                                lds_c(ownD + dB0 + unsigned(od), T()));
+                else
+                    dr = lds_c(ownD + dB0 + unsigned(od), T());   // edge / outside: never read
             } else {
                 const C yc = lds_c(a0 + yB1, T());
                 const C y2 = cadd(yc, yc);
@@ -789,27 +878,28 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         T fi = tfma(hc.a, L.x, sr * yc.x);
         if (hasV) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
         C F; F.x = fr; F.y = fi;
-        if (z == fz_lo || z == fz_hi) {
+        if (shell) A.fp[int64_t(z) * A.per2 + shell_i] = F;
+        if (ok && (z == fz_lo || z == fz_hi)) {
             if (z == fz_lo) A.fz[gy * nx + gx] = F;
             if (z == fz_hi) A.fz[int64_t(nx) * g.ny + gy * nx + gx] = F;
         }
         C o;
         if (STAGE == 1) {
-            *kp = F;
+            if (ok) *kp = F;
             o = cfma(hc.kc, F, yc);
         } else if (STAGE == 4) {
             o = cfma(hc.kc, cadd(kt, F), psi);
         } else {
-            *kp = cfma(T(2), F, kt);
+            if (ok) *kp = cfma(T(2), F, kt);
             o = cfma(hc.kc, F, psi);
         }
-        *outp = o;
-        if (peers) {                                    // slab mode: the neighbours' ghost planes
+        if (ok) *outp = o;
+        if (peers && ok) {                                    // slab mode: the neighbours' ghost planes
             const int64_t q = outp - A.out;
             if (A.peer_lo && z < A.wsend) A.peer_lo[q] = o;
             if (A.peer_hi && z >= nz - A.wsend) A.peer_hi[q] = o;
         }
-        if (STAGE == 4 && !(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
+        if (STAGE == 4 && ok && !(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
         outp += sz;
         kp += sz;
         // queue update and slot rotation
@@ -871,9 +961,18 @@ stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUte
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     // every owned and ring point in-plane interior -> branch-free path
     const bool edge = force_edge || !(x0 >= 2 && x0 + Cfg::TX <= nx - 2 && y0 >= 2 && y0 + Cfg::TY <= ny - 2);
-    if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
-    else if constexpr (ORDER == ORDER_2SHOC) t3_fast<T, BC, STAGE, P, TYV>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
-    else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    // edge tiles without a face point on their ring run the lean loop with face handling;
+    // force_edge == 2 keeps them on the per-point face path (measurement / tests)
+    // (x0 == nx - 1: the x-face point's b' is on the previous tile, out of shuffle reach)
+    const bool lean_edge = force_edge != 2 && x0 + Cfg::TX != nx - 1 && y0 + Cfg::TY != ny - 1 && x0 != nx - 1;
+    if constexpr (ORDER == ORDER_2SHOC) {
+        if (!edge) t3_fast<T, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+        else if (lean_edge) t3_fast<T, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+        else t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    } else {
+        if (edge) t3_run<T, ORDER, BC, STAGE, P, TYV, true>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+        else t3_run<T, ORDER, BC, STAGE, P, TYV, false>(&mY, &mP, &mK, &mV, A, smem_raw, x0, y0, zs, ze);
+    }
 }
 
 }  // namespace nlse

@@ -22,7 +22,7 @@ def _k(ndim, h, scheme):
     return 0.5 * kb
 
 
-@pytest.mark.parametrize("kernel", ["fast", "v1", "generic"])
+@pytest.mark.parametrize("kernel", ["fast", "edge_lean", "edge_pp", "v1", "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
@@ -31,10 +31,12 @@ def _k(ndim, h, scheme):
 def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch):
     """Every kernel family against the oracle: "fast" = the default (3D: TMA z-streaming),
     "v1" = the cp.async z-streaming kernel (3D), "generic" = one thread per point."""
-    if kernel == "v1" and ndim != 3:
-        pytest.skip("v1 is a 3D kernel")
+    if kernel != "fast" and kernel != "generic" and ndim != 3:
+        pytest.skip(f"{kernel} is a 3D kernel variant")
     if kernel == "v1":
         monkeypatch.setenv("NLSE_3D_KERNEL", "v1")
+    if kernel.startswith("edge"):       # every TMA tile on the lean face-aware loop / per-point face path
+        monkeypatch.setenv("NLSE_FORCE_EDGE", "1" if kernel == "edge_lean" else "2")
     generic = kernel == "generic"
     dims = DIMS[ndim]
     h = H[ndim]
@@ -46,10 +48,28 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
     want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+            "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma",
             "generic": "stage_generic"}[kernel]
-    if not (kernel == "fast" and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
+    if not (kernel in ("fast", "edge_lean", "edge_pp") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
         assert info["variant"] == want, info
     assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV} {info['variant']}")
+
+
+@pytest.mark.parametrize("dims", [(65, 33, 9), (33, 17, 7), (64, 31, 8), (97, 49, 6), (63, 47, 7), (35, 20, 6)])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_tile_alignment_cases(dims, bc, precision):
+    """3D grids whose faces fall on every tile position the TMA kernel distinguishes: a face one
+    past a tile (nx = 32k + 1, ny = 16k + 1: the face is on the neighbour tile's ring), a face on
+    lane 0 of a tile (x-face b' on the previous tile), faces on the last lane / row, ragged."""
+    psi0 = case_input(dims, seed=77)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=78))
+    h = 0.5
+    k = _k(3, h, "2shoc")
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme="2shoc", precision=precision)
+    ref = run_oracle(dims, h, psi0, k, 6, **kw)
+    got = run_gpu(dims, h, psi0, k, 6, **kw)
+    assert_parity(got, ref, precision, what=f"{dims} {bc} {precision}")
 
 
 @pytest.mark.parametrize("dims", [(3,), (4,), (3, 3), (3, 5), (5, 3), (3, 3, 3), (4, 3, 5), (3, 7, 3), (9, 3, 4)])
