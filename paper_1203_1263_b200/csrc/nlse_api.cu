@@ -91,7 +91,7 @@ struct nlse_ctx {
     int diag_blocks = 0;
     cudaStream_t stream = nullptr;
     std::shared_ptr<StreamHolder> stream_ref;   // virtual ranks of one group share one stream
-    cudaStream_t side_stream = nullptr;          // 3D boundary kernel, forked / joined per stage
+    cudaStream_t side_stream = nullptr;          // 2D/3D boundary kernel, forked / joined per stage
     cudaStream_t io_stream = nullptr;            // nlse_run_frames downloads
     void *snap[2] = {nullptr, nullptr};          // nlse_run_frames: double2 snapshots of Psi
     cudaEvent_t ev_snap[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
@@ -308,10 +308,11 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
         stage_generic<T, DIM, ORDER, BC, STAGE><<<blocks_for(c->g.n, 256), 256, 0, c->stream>>>(A);
         return;
     }
-    // 3D: the boundary kernel (disjoint outputs, same inputs) runs concurrently on a side
-    // stream, forked from and joined back into the context stream (not in timing mode, so
-    // that per-kernel shares stay attributable)
-    const bool side = DIM == 3 && !c->timing && c->side_stream && !c->fp;
+    // 2D/3D: the boundary kernel (disjoint outputs, same inputs: it recomputes what it needs at
+    // b') runs concurrently on a side stream, forked from and joined back into the context
+    // stream (not in timing mode, so that per-kernel shares stay attributable).  The 3D MSD
+    // light pass (c->fp: F(b') stored by the interior kernel) must follow the interior kernel.
+    const bool side = DIM >= 2 && !c->timing && c->side_stream && !c->fp;
     if (side) {
         const int64_t nb = n_boundary_points<DIM>(c->g);
         cudaEventRecord(c->ev_fork, c->stream);
@@ -760,7 +761,7 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->stream_ref = std::make_shared<StreamHolder>();
     CREATE_TRY(cudaStreamCreateWithFlags(&c->stream_ref->s, cudaStreamNonBlocking));
     c->stream = c->stream_ref->s;
-    if (ndim == 3) {
+    if (ndim >= 2) {
         CREATE_TRY(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
         CREATE_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CREATE_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -820,7 +821,14 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         // TMA needs 16-byte row strides (complex rows: nx even for fp32; V rows: nx*sizeof(T) % 16)
         if (!ok) c->interior_kind = KK_STREAM3D;
         c->tma = ok;
-        if (ok && bc == NLSE_BC_MSD && c->g.nx >= 5 && c->g.ny >= 5) {
+        // MSD: the interior kernel stores F(b') and a light pass after it forms the boundary
+        // outputs.  Recomputing the two-step Laplacian at b' instead costs ~0.8 ms per stage at
+        // 1024^3, and even at 87x87x203, where that kernel could run concurrently on the side
+        // stream, it is slower (17.5 us on the few SMs the interior kernel leaves free vs the
+        // serial 8.3 us light pass: 194 vs 150 us/step, r01 probe2).  NLSE_MSD_FB=0: recompute.
+        const char *efb = getenv("NLSE_MSD_FB");
+        const bool want_fb = !(efb && efb[0] == '0');
+        if (ok && want_fb && bc == NLSE_BC_MSD && c->g.nx >= 5 && c->g.ny >= 5) {
             c->per2 = int(2 * (c->g.nx - 2) + 2 * (c->g.ny - 4));
             const size_t fzb = size_t(2) * size_t(c->g.sz) * cb, fpb = size_t(c->g.nz) * size_t(c->per2) * cb;
             CREATE_TRY(cudaMalloc(&c->fz, fzb));
