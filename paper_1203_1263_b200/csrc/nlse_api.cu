@@ -42,6 +42,10 @@ struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
 #ifndef NLSE_TMA_P
 #define NLSE_TMA_P 3
 #endif
+#ifndef NLSE_TMA_P1
+#define NLSE_TMA_P1 3
+#endif
+constexpr int TMA_P1 = NLSE_TMA_P1;  // ... for stage 1 (Y and V only: a deeper Y ring fits)
 constexpr int TMA_P = NLSE_TMA_P;  // TMA ring prefetch depth of the Y planes (planes ahead; 2 and 4 measured slower, r01 ab1)
 constexpr int GRAPH_STEPS = 8;  // RK4 steps per captured CUDA graph
 
@@ -248,7 +252,8 @@ int obuf_of_stage(int stage) { return stage == 1 ? BUF_TMP : (stage == 2 ? BUF_O
 
 template <typename T, int ORDER, int BC, int STAGE, int TYV>
 void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
-    using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
+    constexpr int PS = STAGE == 1 ? TMA_P1 : TMA_P;
+    using Cfg = T3Cfg<T, ORDER, PS, TYV, STAGE != 1>;
     const int64_t nx = A.g.nx, ny = A.g.ny;
     const int64_t mz = A.g.nz - A.g.zf_lo - A.g.zf_hi;
     const unsigned gx = unsigned((nx + Cfg::TX - 1) / Cfg::TX);
@@ -259,9 +264,9 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     const int64_t cols = int64_t(gx) * gy;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, PS, TYV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, PS, TYV>,
                                                       Cfg::NT, Cfg::SMEM);
         if (per_sm < 1) per_sm = 1;
     }
@@ -288,7 +293,7 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     // loop, =2 every tile on the per-point face path (t3_run, EDGE)
     const char *fe = getenv("NLSE_FORCE_EDGE");
     const int force_edge = (fe && (fe[0] == '1' || fe[0] == '2')) ? fe[0] - '0' : 0;
-    stage3d_tma<T, ORDER, BC, STAGE, TMA_P, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
+    stage3d_tma<T, ORDER, BC, STAGE, PS, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
         c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
         force_edge);
 }

@@ -83,7 +83,9 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap *map
 }
 
 // ------------------------------------------------------------------ configuration
-template <typename T, int ORDER, int P, int TYV = 8>
+// PK: Psi and K_tot are staged (stages 2-4); stage 1 streams only Y and V, and spends the
+// shared memory on a deeper Y ring instead (P = TMA_P1 for stage 1)
+template <typename T, int ORDER, int P, int TYV = 8, bool PK = true>
 struct T3Cfg {
     static constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
     // x halo of the staged tile: a TMA box must start on a 16-byte boundary, so fp32 tiles
@@ -107,7 +109,8 @@ struct T3Cfg {
     static constexpr int YBYTES = PX * PY * CB;
     static constexpr int YSLOT = up128(YBYTES);
     static constexpr int OWN_C = NT * CB, OWN_R = NT * int(sizeof(T));
-    static constexpr int PKVSLOT = up128(2 * OWN_C + OWN_R);          // Psi | K_tot | V
+    static constexpr int VOFF = PK ? 2 * OWN_C : 0;                    // V after Psi | K_tot
+    static constexpr int PKVSLOT = up128(VOFF + OWN_R);                // [Psi | K_tot |] V
     static constexpr int DSLOT = up128(DPX * DPY * CB);
     static constexpr int OFF_PKV = NS * YSLOT;
     static constexpr int OFF_D = OFF_PKV + NP * PKVSLOT;
@@ -129,7 +132,7 @@ struct Tma3Maps {
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV, bool EDGE>
 struct T3Body {
     using C = cplx<T>;
-    using Cfg = T3Cfg<T, ORDER, P, TYV>;
+    using Cfg = T3Cfg<T, ORDER, P, TYV, STAGE != 1>;
     static constexpr int H = Cfg::H, HX = Cfg::HX, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS;
     static constexpr int NP = Cfg::NP, DPX = Cfg::DPX;
 
@@ -251,7 +254,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
                                        const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
                                        int y0, int zs, int ze) {
     using C = cplx<T>;
-    using Cfg = T3Cfg<T, ORDER, P, TYV>;
+    using Cfg = T3Cfg<T, ORDER, P, TYV, STAGE != 1>;
     using B = T3Body<T, ORDER, BC, STAGE, P, TYV, EDGE>;
     constexpr int H = Cfg::H, TX = Cfg::TX, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
     const B b{A, sm, x0, y0};
@@ -288,14 +291,14 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
                 tma_load_3d_hint(smem_u32(dst), mP, 2 * x0, y0, p + g.zghost, bar, pol);
                 tma_load_3d_hint(smem_u32(dst + Cfg::OWN_C), mK, 2 * x0, y0, p, bar, pol);
             }
-            if (A.V) tma_load_3d_hint(smem_u32(dst + 2 * Cfg::OWN_C), mV, x0, y0, p, bar, pol);
+            if (A.V) tma_load_3d_hint(smem_u32(dst + Cfg::VOFF), mV, x0, y0, p, bar, pol);
             return;
         }
         if (STAGE != 1) {
             tma_load_3d(smem_u32(dst), mP, 2 * x0, y0, p + g.zghost, bar);
             tma_load_3d(smem_u32(dst + Cfg::OWN_C), mK, 2 * x0, y0, p, bar);
         }
-        if (A.V) tma_load_3d(smem_u32(dst + 2 * Cfg::OWN_C), mV, x0, y0, p, bar);
+        if (A.V) tma_load_3d(smem_u32(dst + Cfg::VOFF), mV, x0, y0, p, bar);
     };
     // the TMA issuer: lane 0 of the last warp (no ring work there)
     const bool issuer = (tid == Cfg::NT - 32);
@@ -345,7 +348,7 @@ __device__ __forceinline__ void t3_run(const CUtensorMap *mY, const CUtensorMap 
             psi = reinterpret_cast<const C *>(src)[pown];
             kt = reinterpret_cast<const C *>(src + Cfg::OWN_C)[pown];
         }
-        if (A.V) v = reinterpret_cast<const T *>(src + 2 * Cfg::OWN_C)[pown];
+        if (A.V) v = reinterpret_cast<const T *>(src + Cfg::VOFF)[pown];
     };
 
     if (ORDER == ORDER_CD) {
@@ -579,7 +582,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
                                         const CUtensorMap *mV, const StageArgs<T> &A, unsigned char *sm, int x0,
                                         int y0, int zs, int ze) {
     using C = cplx<T>;
-    using Cfg = T3Cfg<T, ORDER_2SHOC, P, TYV>;
+    using Cfg = T3Cfg<T, ORDER_2SHOC, P, TYV, STAGE != 1>;
     using B = T3Body<T, ORDER_2SHOC, BC, STAGE, P, TYV, false>;
     constexpr int H = Cfg::H, TX = Cfg::TX, TY = Cfg::TY, PX = Cfg::PX, NS = Cfg::NS, NP = Cfg::NP, DPX = Cfg::DPX;
     constexpr int CB = Cfg::CB;
@@ -616,7 +619,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
             tma_load_3d(dst, mP, 2 * x0, y0, p + g.zghost, bar);
             tma_load_3d(dst + Cfg::OWN_C, mK, 2 * x0, y0, p, bar);
         }
-        if (hasV) tma_load_3d(dst + 2 * Cfg::OWN_C, mV, x0, y0, p, bar);
+        if (hasV) tma_load_3d(dst + Cfg::VOFF, mV, x0, y0, p, bar);
     };
     const unsigned cbar0 = bar0 + 8 * (NS + NP);
     if (tid == 0) {
@@ -649,7 +652,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
     const unsigned ownY = sb + unsigned(((ty + H) * PX + tx + Cfg::HX) * CB);
     const unsigned ownD = sb + unsigned(Cfg::OFF_D + ((ty + 1) * DPX + tx + 1) * CB);
     const unsigned ownP = sb + unsigned(Cfg::OFF_PKV + (ty * TX + tx) * CB);
-    const unsigned ownV = sb + unsigned(Cfg::OFF_PKV + 2 * Cfg::OWN_C + (ty * TX + tx) * int(sizeof(T)));
+    const unsigned ownV = sb + unsigned(Cfg::OFF_PKV + Cfg::VOFF + (ty * TX + tx) * int(sizeof(T)));
     auto ldY = [&](unsigned slotB, int d) -> C { return lds_c(ownY + slotB + unsigned(d * CB), T()); };
     // ring duty: role 0 = row -1, 1 = row TY, 2 = columns -1 and TX (2 TY lanes), 3 = none;
     // role of warp ty in iteration jj = (ty - jj) mod TY with rotation, ty without
@@ -947,7 +950,7 @@ __global__ void __launch_bounds__(32 * TYV, (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3)
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
             const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge) {
-    using Cfg = T3Cfg<T, ORDER, P, TYV>;
+    using Cfg = T3Cfg<T, ORDER, P, TYV, STAGE != 1>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int ntiles = ntx * nty;
     const int w = blockIdx.x;
