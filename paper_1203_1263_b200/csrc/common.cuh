@@ -94,6 +94,9 @@ template <typename T> struct StageArgs {
     int per2;
     int stream_hints;     // 1: L2 evict-first hints on the once-per-stage streams (measured slower, off)
     int ring_rot;         // 1: rotate the 3D ring-D duty over the warps plane by plane
+    int xfuse;            // 3D MSD light-pass mode: the x-face points with 1 <= j <= ny-2 of the
+                          // interior planes are finished by the stage kernel (F(b') by a lane
+                          // shuffle); the light pass covers the z faces and the y-face rows only
 };
 
 // Index of an in-plane point one step in from the x/y faces (nx, ny >= 5), in the order:

@@ -183,8 +183,11 @@ __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
 // 1D: 2 points; 2D: the 2(nx + ny) - 4 perimeter; 3D: the global z faces this grid
 // owns (plane 0 if zf_lo, plane nz-1 if zf_hi), then the perimeter of every other
 // owned plane.
+// rows_only (3D): the interior planes contribute their two y-face rows only (the x-face
+// points of those planes are finished elsewhere: StageArgs::xfuse).
 template <int DIM>
-__device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i, int64_t &j, int64_t &k) {
+__device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i, int64_t &j, int64_t &k,
+                                          bool rows_only = false) {
     // 32-bit index arithmetic (64-bit division is a long software sequence on the GPU); the
     // launch checks that the boundary count and a face fit in 31 bits
     const unsigned nx = unsigned(g.nx), ny = unsigned(g.ny);
@@ -194,7 +197,7 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
         i = t ? g.nx - 1 : 0; j = 0; k = 0;
         return true;
     }
-    const unsigned per = 2u * nx + 2u * (ny - 2u);    // perimeter of one xy plane
+    const unsigned per = 2u * nx + (rows_only ? 0u : 2u * (ny - 2u));   // perimeter of one xy plane
     auto perim = [&](unsigned u, int64_t &ii, int64_t &jj) {
         if (u < nx) { ii = u; jj = 0; }
         else if (u < 2u * nx) { ii = u - nx; jj = ny - 1u; }
@@ -223,9 +226,9 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
 }
 
 template <int DIM>
-inline int64_t n_boundary_points(const Grid &g) {
+inline int64_t n_boundary_points(const Grid &g, bool rows_only = false) {
     if (DIM == 1) return 2;
-    const int64_t per = 2 * g.nx + 2 * (g.ny - 2);
+    const int64_t per = 2 * g.nx + (rows_only ? 0 : 2 * (g.ny - 2));
     if (DIM == 2) return per;
     const int nf = g.zf_lo + g.zf_hi;
     return nf * g.nx * g.ny + per * (g.nz - nf);
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(256) stage_boundary_msd_fb(StageArgs<T> A) {
     using C = cplx<T>;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     int64_t i, j, k;
-    if (!bnd_point<3>(A.g, t, i, j, k)) return;
+    if (!bnd_point<3>(A.g, t, i, j, k, A.xfuse != 0)) return;
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     const int i1 = i == 0 ? 1 : (i == nx - 1 ? nx - 2 : int(i));
     const int j1 = j == 0 ? 1 : (j == ny - 1 ? ny - 2 : int(j));

@@ -230,6 +230,19 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
     return r == CUDA_SUCCESS;
 }
 
+// The stage kernel finishes the x-face boundary points itself (StageArgs::xfuse) when every
+// tile that owns x-face points runs the lean face-aware loop (t3_lean_ok in stage3d_tma.cuh:
+// no face point on a tile's ring, no x face on lane 0 of a tile past x = 0).
+bool xfuse_mode(const nlse_ctx *c) {
+    if (!c->tma || !c->fp || c->order != NLSE_2SHOC4) return false;
+    const char *fe = getenv("NLSE_FORCE_EDGE");
+    if (fe && fe[0] == '2') return false;
+    const char *ex = getenv("NLSE_XFUSE");
+    if (ex && ex[0] == '0') return false;
+    const int64_t nx = c->g.nx, ny = c->g.ny;
+    return (nx - 1) % 32 != 0 && (ny - 1) % c->tma_ty != 0;
+}
+
 template <typename T, int ORDER, int TYV>
 bool build_maps(nlse_ctx *c) {
     using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
@@ -342,7 +355,7 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
         cudaStreamWaitEvent(c->stream, c->ev_join, 0);
     } else if (DIM == 3 && BC == BC_MSD && A.fp) {
         // F(b') was stored by the interior kernel: a light pass after it
-        const int64_t nb = n_boundary_points<DIM>(c->g);
+        const int64_t nb = n_boundary_points<DIM>(c->g, A.xfuse != 0);
         LaunchTimer lt(c, KK_BOUNDARY, nb);
         stage_boundary_msd_fb<T, STAGE><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
     } else {
@@ -396,6 +409,7 @@ void enqueue_stage_t(nlse_ctx *c, int stage, double k, int step) {
     A.fz = (C *)c->fz;
     A.fp = (C *)c->fp;
     A.per2 = c->per2;
+    A.xfuse = xfuse_mode(c) ? 1 : 0;
     // (RK4_GPU) P:495-519: stages {1-3}, {4-6}, {7-9}, {10-11}
     switch (stage) {
         case 1: launch_stage<T, DIM, ORDER, BC, 1>(c, A); break;

@@ -675,6 +675,7 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
     const bool fpz = A.fp != nullptr;
     const int fz_lo = (fpz && g.zf_lo) ? 1 : INT32_MIN, fz_hi = (fpz && g.zf_hi) ? nz - 2 : INT32_MIN;
     const bool peers = A.peer_lo != nullptr || A.peer_hi != nullptr;
+    const bool xfuse = BC == BC_MSD && A.xfuse != 0;
     // face points: V at b and b' of a plane (global, read one plane ahead; planes outside
     // [0, nz) have no V and their face D is never read)
     const bool vface = (xf || yf) && hasV && BC != BC_L0;
@@ -886,23 +887,41 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
             if (z == fz_lo) A.fz[gy * nx + gx] = F;
             if (z == fz_hi) A.fz[int64_t(nx) * g.ny + gy * nx + gx] = F;
         }
+        if (EDGE && xfuse) {
+            // x-face points of this plane, (msd) P:331-335: F_b = i Im(F_b'/Y_b') Y_b with b' the
+            // neighbouring lane (same arithmetic as stage_boundary_msd_fb)
+            const unsigned full = 0xffffffffu;
+            C f1, y1;
+            f1.x = __shfl_sync(full, F.x, srcl);
+            f1.y = __shfl_sync(full, F.y, srcl);
+            y1.x = __shfl_sync(full, yc.x, srcl);
+            y1.y = __shfl_sync(full, yc.y, srcl);
+            if (xf) {
+                const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+                T m = T(0);
+                if (!(rho1 < A.c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
+                F.x = -(m * yc.y);
+                F.y = m * yc.x;
+            }
+        }
         C o;
+        const bool okw = ok || (EDGE && xfuse && xf);   // points this thread writes
         if (STAGE == 1) {
-            if (ok) *kp = F;
+            if (okw) *kp = F;
             o = cfma(hc.kc, F, yc);
         } else if (STAGE == 4) {
             o = cfma(hc.kc, cadd(kt, F), psi);
         } else {
-            if (ok) *kp = cfma(T(2), F, kt);
+            if (okw) *kp = cfma(T(2), F, kt);
             o = cfma(hc.kc, F, psi);
         }
-        if (ok) *outp = o;
-        if (peers && ok) {                                    // slab mode: the neighbours' ghost planes
+        if (okw) *outp = o;
+        if (peers && okw) {                                    // slab mode: the neighbours' ghost planes
             const int64_t q = outp - A.out;
             if (A.peer_lo && z < A.wsend) A.peer_lo[q] = o;
             if (A.peer_hi && z >= nz - A.wsend) A.peer_hi[q] = o;
         }
-        if (STAGE == 4 && ok && !(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
+        if (STAGE == 4 && okw && !(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
         outp += sz;
         kp += sz;
         // queue update and slot rotation

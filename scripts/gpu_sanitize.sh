@@ -2,10 +2,10 @@
 # compute-sanitizer memcheck / racecheck / synccheck / initcheck on small cases of every kernel family.
 out=gpurun_out/sanitize; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-CASES=("70x37x29 2shoc msd fp64 V" "70x37x29 2shoc dirichlet fp32 V" "65x33x9 2shoc msd fp64 V"
+CASES=("70x37x29 2shoc msd fp64 V" "70x37x29 2shoc dirichlet fp32" "64x33x9 2shoc msd fp64 V" "65x33x9 2shoc msd fp64"
        "40x26x22 2shoc l0 fp64" "40x26x22 cd dirichlet fp32" "70x41 2shoc msd fp64 V" "301 2shoc msd fp64")
 for tool in memcheck racecheck synccheck initcheck; do
-  # 70x37x29: interior (lean), lean edge and ragged tiles; 65x33x9: tiles whose ring holds a
+  # 70x37x29: interior (lean), lean edge and ragged tiles; 64x33x9 / 65x33x9: tiles whose ring holds a
   # face point (per-point face path); 40x26x22: all tiles on the lean edge path
   for c in "${CASES[@]}"; do
     NSTEPS=2 timeout 300 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/debug_case.py $c > $out/${tool}_${c// /_}.log 2>&1
