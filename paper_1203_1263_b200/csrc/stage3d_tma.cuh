@@ -41,6 +41,21 @@ __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
+#ifdef NLSE_MBAR_HINT
+// try_wait with a suspend-time hint (ns): the thread sleeps until the phase completes or the
+// hint expires instead of re-polling at the system-dependent default interval (A/B knob)
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "n"(NLSE_MBAR_HINT)
+        : "memory");
+}
+#else
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     asm volatile(
         "{\n"
@@ -52,6 +67,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
