@@ -18,28 +18,60 @@ namespace nlse {
 
 constexpr int T2_TX = 32, T2_TY = 16, T2_NT = 256;
 
+// cp.async (Ampere-style asynchronous copies, global -> shared without a register round
+// trip): every load of the tile and of the owned Psi / K_tot / V is in flight at once
+template <int BYTES>
+__device__ __forceinline__ void t2_cp(void *sdst, const void *gsrc, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    const int n = valid ? BYTES : 0;                  // src-size 0: zero fill
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES), "r"(n)
+                     : "memory");
+}
+__device__ __forceinline__ void t2_cp_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <typename T, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
     using C = cplx<T>;
     constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
     constexpr int PX = T2_TX + 2 * H, PY = T2_TY + 2 * H;
     constexpr int DPX = T2_TX + 2, DPY = T2_TY + 2;
-    __shared__ C ys[PY * PX];
-    __shared__ C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
+    __shared__ __align__(16) C ys[PY * PX];
+    __shared__ __align__(16) C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
+    __shared__ __align__(16) C ps[STAGE != 1 ? 2 * T2_NT : 1], ks[STAGE != 1 ? 2 * T2_NT : 1];
+    __shared__ __align__(16) T vs[2 * T2_NT];
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     const int x0 = blockIdx.x * T2_TX, y0 = blockIdx.y * T2_TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
 
-    // (1) Y tile with halo (zero outside the grid; those values are never used)
+    // (1) Y tile with halo (zero outside the grid; those values are never used), and Psi,
+    // K_tot, V of the owned points, all as asynchronous copies
     for (int ly = ty - H; ly < T2_TY + H; ly += T2_NT / 32) {
         const int gy = y0 + ly;
         for (int lx = tx - H; lx < T2_TX + H; lx += 32) {
             const int gx = x0 + lx;
-            C v; v.x = T(0); v.y = T(0);
-            if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) v = __ldg(A.Y + int64_t(gy) * A.g.sy + gx);
-            ys[(ly + H) * PX + (lx + H)] = v;
+            const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+            t2_cp<int(sizeof(C))>(&ys[(ly + H) * PX + (lx + H)], A.Y + (in ? int64_t(gy) * A.g.sy + gx : 0), in);
         }
     }
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const int gx = x0 + tx, gy = y0 + ty + 8 * r;
+        if (gx >= 1 && gx <= nx - 2 && gy >= 1 && gy <= ny - 2) {
+            const int64_t q = int64_t(gy) * A.g.sy + gx;
+            if (STAGE != 1) {
+                t2_cp<int(sizeof(C))>(&ps[r * T2_NT + tid], A.Psi + q, true);
+                t2_cp<int(sizeof(C))>(&ks[r * T2_NT + tid], A.K + q, true);
+            }
+            if (A.V) t2_cp<int(sizeof(T))>(&vs[r * T2_NT + tid], A.V + q, true);
+        }
+    }
+    t2_cp_wait_all();
     __syncthreads();
     auto Ys = [&](int lx, int ly) -> C { return ys[(ly + H) * PX + (lx + H)]; };
     auto D_int = [&](int lx, int ly) -> C {
@@ -56,8 +88,16 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         return n;
     };
 
-    // (2) 2SHOC step 1 over the tile + ring
-    if (ORDER == ORDER_2SHOC) {
+    // (2) 2SHOC step 1 over the tile + ring.  Tiles whose ring is in-grid interior (the
+    // bulk of a large grid) take the stencil everywhere, without per-point face tests.
+    const bool inner = x0 >= 2 && x0 + T2_TX <= nx - 2 && y0 >= 2 && y0 + T2_TY <= ny - 2;
+    if (ORDER == ORDER_2SHOC && inner) {
+        for (int e = tid; e < DPX * DPY; e += T2_NT) {
+            const int lx = e % DPX - 1, ly = e / DPX - 1;
+            ds[e] = D_int(lx, ly);
+        }
+        __syncthreads();
+    } else if (ORDER == ORDER_2SHOC) {
         for (int e = tid; e < DPX * DPY; e += T2_NT) {
             const int lx = e % DPX - 1, ly = e / DPX - 1;
             const int gx = x0 + lx, gy = y0 + ly;
@@ -121,13 +161,23 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
         T fi = tfma(A.c.a, L.x, sr * yc.x);
         if (A.V) {
-            const T v = __ldg(A.V + q);
+            const T v = vs[r * T2_NT + tid];
             fr = tfma(v, yc.y, fr);
             fi = tfma(-v, yc.x, fi);
         }
         C F; F.x = fr; F.y = fi;
-        const C psi = (STAGE == 1) ? yc : A.Psi[q];
-        rk_combine<STAGE, T>(A, q, 0, F, psi);
+        // RK4 stage combine (RK4_GPU) P:495-519, as rk_combine with Psi, K_tot staged
+        if (STAGE == 1) {
+            A.K[q] = F;
+            store_out(A, q, 0, cfma(A.c.kc, F, yc));
+        } else if (STAGE == 4) {
+            const C o = cfma(A.c.kc, cadd(ks[r * T2_NT + tid], F), ps[r * T2_NT + tid]);
+            store_out(A, q, 0, o);
+            if (!(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
+        } else {
+            A.K[q] = cfma(T(2), F, ks[r * T2_NT + tid]);
+            store_out(A, q, 0, cfma(A.c.kc, F, ps[r * T2_NT + tid]));
+        }
     }
 }
 
