@@ -240,7 +240,12 @@ bool xfuse_mode(const nlse_ctx *c) {
     const char *ex = getenv("NLSE_XFUSE");
     if (ex && ex[0] == '0') return false;
     const int64_t nx = c->g.nx, ny = c->g.ny;
-    return (nx - 1) % 32 != 0 && (ny - 1) % c->tma_ty != 0;
+    if ((nx - 1) % 32 == 0 || (ny - 1) % c->tma_ty == 0) return false;
+    // worth it where the light pass is bandwidth-bound on the scattered x-face points (1024^3:
+    // 2.1M of them, -0.6 % step time); on small grids the edge tiles are the critical path
+    // (87x87x203: 161 vs 150 us/step with it), so only from 2^18 x-face points on (or =1)
+    if (ex && ex[0] == '1') return true;
+    return 2 * (ny - 2) * (c->g.nz - c->g.zf_lo - c->g.zf_hi) >= (int64_t(1) << 18);
 }
 
 template <typename T, int ORDER, int TYV>

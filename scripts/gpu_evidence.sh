@@ -22,4 +22,7 @@ if [ "${SRC:-1}" = "1" ]; then
   ncu -i $out/src.ncu-rep --page source --csv --print-source sass > $out/sass.csv 2>/dev/null
   rm -f $out/src.ncu-rep
 fi
+if [ "${CONFIGS:-0}" = "1" ]; then
+  timeout 900 python scripts/bench_configs.py --json $out/configs.json > $out/configs.txt 2>&1; echo "configs rc=$?"
+fi
 ls -la $out

@@ -22,7 +22,8 @@ def _k(ndim, h, scheme):
     return 0.5 * kb
 
 
-@pytest.mark.parametrize("kernel", ["fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "v1", "generic"])
+@pytest.mark.parametrize("kernel", ["fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on", "v1",
+                                    "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
@@ -39,10 +40,10 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
         if bc != "msd":
             pytest.skip("MSD only")
         monkeypatch.setenv("NLSE_MSD_FB", "0")
-    if kernel == "xfuse_off":           # 3D MSD: the light pass also finishes the x-face points
+    if kernel in ("xfuse_off", "xfuse_on"):   # 3D MSD: x-face points by the light pass / the stage kernel
         if bc != "msd":
             pytest.skip("MSD only")
-        monkeypatch.setenv("NLSE_XFUSE", "0")
+        monkeypatch.setenv("NLSE_XFUSE", "0" if kernel == "xfuse_off" else "1")
     if kernel.startswith("edge"):       # every TMA tile on the lean face-aware loop / per-point face path
         monkeypatch.setenv("NLSE_FORCE_EDGE", "1" if kernel == "edge_lean" else "2")
     generic = kernel == "generic"
@@ -56,9 +57,9 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
     want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
-            "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma", "msd_recompute": "stage3d_tma", "xfuse_off": "stage3d_tma",
+            "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma", "msd_recompute": "stage3d_tma", "xfuse_off": "stage3d_tma", "xfuse_on": "stage3d_tma",
             "generic": "stage_generic"}[kernel]
-    if not (kernel in ("fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
+    if not (kernel in ("fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
         assert info["variant"] == want, info
     assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV} {info['variant']}")
 

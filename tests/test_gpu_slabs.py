@@ -34,16 +34,16 @@ def test_slabs_bitwise_equal_single(scheme, bc, precision, nranks):
     assert ulp_diff(many, one, precision) == 0
 
 
-@pytest.mark.parametrize("kernel", ["v1", "generic", "msd_recompute", "xfuse_off", "edge_lean", "edge_pp"])
+@pytest.mark.parametrize("kernel", ["v1", "generic", "msd_recompute", "xfuse_on", "edge_lean", "edge_pp"])
 def test_slabs_other_kernel_families(kernel, monkeypatch):
-    dims = (40, 33, 24)
+    dims = (40, 35, 24)          # (nx-1) % 32 != 0 and (ny-1) % 16 != 0: xfuse can apply
     psi0 = case_input(dims, seed=43)
     if kernel == "v1":
         monkeypatch.setenv("NLSE_3D_KERNEL", "v1")
     if kernel == "msd_recompute":        # boundary kernel recomputes F(b') (no light pass)
         monkeypatch.setenv("NLSE_MSD_FB", "0")
-    if kernel == "xfuse_off":
-        monkeypatch.setenv("NLSE_XFUSE", "0")
+    if kernel == "xfuse_on":
+        monkeypatch.setenv("NLSE_XFUSE", "1")
     if kernel.startswith("edge"):
         monkeypatch.setenv("NLSE_FORCE_EDGE", "1" if kernel == "edge_lean" else "2")
     kw = dict(s=-1.0, bc="msd", scheme="2shoc", generic=kernel == "generic")
