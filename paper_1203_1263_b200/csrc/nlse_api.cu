@@ -224,9 +224,17 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
     cuuint64_t strides[2] = {d0 * uint64_t(eb), d0 * d1 * uint64_t(eb)};
     cuuint32_t box[3] = {b0, b1, 1}, estr[3] = {1, 1, 1};
     if (strides[0] % 16 || strides[1] % 16) return false;
+    // L2 promotion of the TMA reads: NLSE_TMA_L2PROMO = 0 (none) / 64 / 128 / 256 (default) bytes
+    static const CUtensorMapL2promotion promo = [] {
+        const char *e = getenv("NLSE_TMA_L2PROMO");
+        const int v = e ? std::atoi(e) : 256;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                      : (v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                 : (v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B));
+    }();
     CUresult r = enc(m, eb == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 

@@ -16,7 +16,11 @@
 
 namespace nlse {
 
-constexpr int T2_TX = 32, T2_TY = 16, T2_NT = 256;
+#ifndef NLSE_T2_TY
+#define NLSE_T2_TY 16
+#endif
+constexpr int T2_TX = 32, T2_TY = NLSE_T2_TY, T2_NT = 256;
+constexpr int T2_RPT = T2_TY / 8;          // rows per thread (8 warps)
 
 // cp.async (Ampere-style asynchronous copies, global -> shared without a register round
 // trip): every load of the tile and of the owned Psi / K_tot / V is in flight at once
@@ -43,8 +47,8 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
     constexpr int DPX = T2_TX + 2, DPY = T2_TY + 2;
     __shared__ __align__(16) C ys[PY * PX];
     __shared__ __align__(16) C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
-    __shared__ __align__(16) C ps[STAGE != 1 ? 2 * T2_NT : 1], ks[STAGE != 1 ? 2 * T2_NT : 1];
-    __shared__ __align__(16) T vs[2 * T2_NT];
+    __shared__ __align__(16) C ps[STAGE != 1 ? T2_RPT * T2_NT : 1], ks[STAGE != 1 ? T2_RPT * T2_NT : 1];
+    __shared__ __align__(16) T vs[T2_RPT * T2_NT];
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     const int x0 = blockIdx.x * T2_TX, y0 = blockIdx.y * T2_TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -60,7 +64,7 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         }
     }
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
+    for (int r = 0; r < T2_RPT; r++) {
         const int gx = x0 + tx, gy = y0 + ty + 8 * r;
         if (gx >= 1 && gx <= nx - 2 && gy >= 1 && gy <= ny - 2) {
             const int64_t q = int64_t(gy) * A.g.sy + gx;
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
 
     // (3) step 2, F, RK4 stage combine at the owned interior points
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
+    for (int r = 0; r < T2_RPT; r++) {
         const int lx = tx, ly = ty + 8 * r;
         const int gx = x0 + lx, gy = y0 + ly;
         if (gx < 1 || gx > nx - 2 || gy < 1 || gy > ny - 2) continue;
