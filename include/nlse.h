@@ -102,8 +102,10 @@ nlse_status nlse_get_psi_device(nlse_ctx *ctx, void *d_psi);
  * nsteps < 0); NLSE_ERR_UNSTABLE if k exceeds the linear bound of
  * nlse_stability_bound and NLSE_FLAG_FORCE_DT was not given; NLSE_ERR_DIVERGED
  * if Psi became non-finite (checked once per step inside the last stage
- * kernel; the state is left as computed).  Results are bitwise independent of
- * how a run is split into nlse_step calls (chunk invariance). */
+ * kernel; the state is left as computed; the report is sticky -- later steps
+ * return it again -- until Psi is replaced by nlse_set_psi / nlse_set_psi_device).
+ * Results are bitwise independent of how a run is split into nlse_step calls
+ * (chunk invariance). */
 nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
 
 /* ---------------------------------------------------------------- slab mode (§8(e))
@@ -117,8 +119,9 @@ nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
  *
  * In slab mode nlse_set_psi*, nlse_step and nlse_diagnostics are COLLECTIVE: every
  * rank calls them in the same order (like NCCL collectives).  Psi / V host buffers
- * hold the local slab (nloc planes).  1D and 2D grids are not partitioned (they run as
- * independent replicas). */
+ * hold the local slab (nloc planes).  Slab mode is for 3D grids only: nlse_create_dist
+ * returns NLSE_ERR_ARG for ndim != 3 (a 1D or 2D job over several GPUs runs one
+ * independent nlse_create context per GPU). */
 #define NLSE_MAX_RANKS 16
 #define NLSE_DIST_HANDLE_BYTES 512
 
@@ -140,8 +143,9 @@ nlse_status nlse_dist_export(nlse_ctx *ctx, void *handle);
 /* Map the peers: `handles` = nranks handles in rank order (this rank's included).
  * NLSE_ERR_COMM if a handle is malformed or cannot be opened. */
 nlse_status nlse_dist_connect(nlse_ctx *ctx, const void *handles);
-/* Virtual ranks: connect the n slab contexts of ONE process (ranks 0..n-1 in order,
- * any devices).  Drive them with the _group calls below. */
+/* Virtual ranks: connect the n slab contexts of ONE process (ranks 0..n-1 in order, all
+ * created on the same device; NLSE_ERR_ARG otherwise).  They share one stream; drive them
+ * with the _group calls below. */
 nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n);
 /* nlse_step / nlse_diagnostics over a group of contexts driven by one host thread
  * (work is enqueued interleaved per stage; mass[j], hamiltonian[j] per context, all

@@ -51,7 +51,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // mode bit 1: signal, bit 2: wait.  Slab mode on separate GPUs launches both in one
 // kernel; virtual ranks sharing one stream launch every rank's signal before any wait
 // (a spinning kernel must never sit in front of the work that releases it).
-__global__ void __launch_bounds__(32) peer_barrier(BarrierArgs b, int mode) {
+static __global__ void __launch_bounds__(32) peer_barrier(BarrierArgs b, int mode) {
     const int t = threadIdx.x;
     const unsigned long long epoch = b.own->my_epoch + ((mode & 1) ? 1ull : 0ull);
     __syncwarp();
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(32) peer_barrier(BarrierArgs b, int mode) {
 }
 
 // Advance the device step counter after a launch sequence of n steps.
-__global__ void add_steps(int *counter, int n) {
+static __global__ void add_steps(int *counter, int n) {
     if (threadIdx.x == 0) *counter += n;
 }
 
@@ -77,7 +77,7 @@ struct PushArgs {
     CommBlock *dst[MAX_RANKS];
     int n, me;
 };
-__global__ void __launch_bounds__(32) diag_push(const double *__restrict__ local, PushArgs a) {
+static __global__ void __launch_bounds__(32) diag_push(const double *__restrict__ local, PushArgs a) {
     const int t = threadIdx.x;
     if (t < a.n) {
         a.dst[t]->xbuf[a.me][0] = local[0];
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(32) diag_push(const double *__restrict__ local
 }
 
 // Sum the nranks partial pairs in rank order (identical on every rank) and scale by h^d.
-__global__ void __launch_bounds__(32) diag_sum(const CommBlock *__restrict__ own, int n, double hd,
+static __global__ void __launch_bounds__(32) diag_sum(const CommBlock *__restrict__ own, int n, double hd,
                                                double *__restrict__ result) {
     if (threadIdx.x == 0) {
         double m = 0.0, e = 0.0;

@@ -1,0 +1,5 @@
+// Stage kernels of one family (precision f32, 2D, 2SHOC): a separate translation unit so
+// that nvcc compiles the families in parallel (stages.cuh).
+#include "stages.cuh"
+
+NLSE_DEFINE_STAGES(f32, 2, shoc)

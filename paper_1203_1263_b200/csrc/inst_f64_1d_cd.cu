@@ -1,0 +1,6 @@
+// Stage kernels of one family (precision f64, 1D, CD): a separate translation unit so
+// that nvcc compiles the families in parallel (stages.cuh).
+#include "stages.cuh"
+
+NLSE_DEFINE_STAGES(f64, 1, cd)
+NLSE_DEFINE_PERSIST1D(f64, cd)

@@ -1,0 +1,5 @@
+// Stage kernels of one family (precision f64, 2D, 2SHOC): a separate translation unit so
+// that nvcc compiles the families in parallel (stages.cuh).
+#include "stages.cuh"
+
+NLSE_DEFINE_STAGES(f64, 2, shoc)

@@ -4,52 +4,25 @@
 // divergence flag, diagnostics (a10) and per-kernel timing.
 #include <unistd.h>
 
-#include <cmath>
-#include <cstdio>
-#include <memory>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <vector>
-
 #include <cudaTypedefs.h>
 
-#include "../../include/nlse.h"
-#include "comm.cuh"
-#include "common.cuh"
+#include "runtime.cuh"
 #include "diag.cuh"
 #include "generic.cuh"
 #include "persist1d.cuh"
 #include "stage3d_tma.cuh"
-#include "stream3d.cuh"
-#include "tile2d.cuh"
 
 using namespace nlse;
+using namespace nlse_rt;
 
 static_assert(NLSE_MAX_RANKS == MAX_RANKS, "rank limits of nlse.h and comm.cuh differ");
 
+thread_local std::string nlse_rt::g_create_error;
+
 namespace {
 
-thread_local std::string g_create_error;
-
-enum KernelKind { KK_GENERIC = 0, KK_STREAM3D, KK_TMA3D, KK_TILE2D, KK_TILE1D, KK_BOUNDARY, KK_DIAG, KK_COMM, KK_COUNT };
 const char *kKindName[KK_COUNT] = {"stage_generic", "stage3d_stream", "stage3d_tma", "stage2d_tile",
                                    "stage1d_tile", "stage_boundary", "diag", "peer_barrier"};
-static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
-
-struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
-
-#ifndef NLSE_TMA_P
-#define NLSE_TMA_P 3
-#endif
-#ifndef NLSE_TMA_P1
-#define NLSE_TMA_P1 3
-#endif
-constexpr int TMA_P1 = NLSE_TMA_P1;  // ... for stage 1 (Y and V only: a deeper Y ring fits)
-constexpr int TMA_P = NLSE_TMA_P;  // TMA ring prefetch depth of the Y planes (planes ahead; 2 and 4 measured slower, r01 ab1)
-constexpr int GRAPH_STEPS = 8;  // RK4 steps per captured CUDA graph
-
-enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2 };
 
 struct DistBlob {               // what nlse_dist_export writes (NLSE_DIST_HANDLE_BYTES)
     uint32_t magic, version;
@@ -60,116 +33,6 @@ struct DistBlob {               // what nlse_dist_export writes (NLSE_DIST_HANDL
 };
 static_assert(sizeof(DistBlob) <= NLSE_DIST_HANDLE_BYTES, "blob too large");
 constexpr uint32_t kBlobMagic = 0x4e4c5345u;  // "NLSE"
-
-}  // namespace
-
-struct StreamHolder {
-    cudaStream_t s = nullptr;
-    ~StreamHolder() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
-};
-
-struct nlse_ctx {
-    int ndim = 0;
-    int64_t dims[3] = {1, 1, 1};    // global grid
-    double h = 0, a = 0, s = 0;
-    nlse_bc bc = NLSE_BC_DIRICHLET;
-    nlse_order order = NLSE_CD2;
-    nlse_precision prec = NLSE_FP64;
-    uint32_t flags = 0;
-    Grid g{};                        // owned grid (the slab in slab mode)
-    int eb = 8;                      // sizeof(real)
-    bool hasV = false;
-    // halo'd buffers: allocation base (plane -zghost) and plane-0 pointer
-    void *alloc[3] = {nullptr, nullptr, nullptr};
-    void *buf[3] = {nullptr, nullptr, nullptr};
-    void *K = nullptr, *V = nullptr;
-    void *fz = nullptr, *fp = nullptr;   // MSD 3D TMA path: stored F(b') (see StageArgs)
-    int per2 = 0;
-    int *d_div = nullptr;
-    int *h_div = nullptr;            // pinned
-    int *d_steps = nullptr;          // device counter of completed steps (divergence report)
-    // CUDA graph of GRAPH_STEPS steps for the current k (nlse_step with many steps)
-    cudaGraphExec_t graph_exec = nullptr;
-    double graph_k = 0;
-    double *d_partial = nullptr, *d_result = nullptr, *h_result = nullptr;
-    int diag_blocks = 0;
-    cudaStream_t stream = nullptr;
-    std::shared_ptr<StreamHolder> stream_ref;   // virtual ranks of one group share one stream
-    cudaStream_t side_stream = nullptr;          // 2D/3D boundary kernel, forked / joined per stage
-    cudaStream_t io_stream = nullptr;            // nlse_run_frames downloads
-    void *snap[2] = {nullptr, nullptr};          // nlse_run_frames: double2 snapshots of Psi
-    cudaEvent_t ev_snap[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    int device = 0;
-    int64_t steps_done = 0;
-    int64_t device_bytes = 0;
-    std::string err;
-    bool sticky = false;
-    bool timing = false;
-    std::vector<TimedLaunch> pending;
-    std::vector<cudaEvent_t> event_pool;
-    double kind_ms[KK_COUNT] = {0};
-    int64_t kind_launches[KK_COUNT] = {0};
-    int64_t kind_points[KK_COUNT] = {0};
-    int interior_kind = KK_GENERIC;
-    bool tma = false;
-    int tma_ty = 8;                  // TMA kernel tile height (8: 256 threads, 16: 512 threads)
-    Tma3Maps maps{};
-    // slab mode
-    bool dist = false;
-    int rank = 0, nranks = 1;
-    int64_t z0 = 0;
-    CommBlock *comm = nullptr;
-    bool connected = false;
-    void *peer_alloc[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [buf][lo, hi]
-    int64_t peer_nloc[2] = {0, 0};
-    CommBlock *peer_comm[MAX_RANKS] = {nullptr};
-    std::vector<void *> ipc_opened;
-    bool ghost_stale = false;
-    bool virtual_group = false;      // connected by nlse_dist_connect_local: _group calls only
-    bool persist1d = false;          // 1D: one persistent CTA per nlse_step call
-};
-
-namespace {
-
-nlse_status fail(nlse_ctx *c, nlse_status st, const std::string &msg) {
-    if (c) {
-        c->err = msg;
-        if (st == NLSE_ERR_CUDA) c->sticky = true;
-    } else {
-        g_create_error = msg;
-    }
-    return st;
-}
-
-#define CUDA_TRY(ctx, expr)                                                                      \
-    do {                                                                                         \
-        cudaError_t e_ = (expr);                                                                 \
-        if (e_ != cudaSuccess)                                                                   \
-            return fail(ctx, e_ == cudaErrorMemoryAllocation ? NLSE_ERR_OOM : NLSE_ERR_CUDA,     \
-                        std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
-    } while (0)
-
-cudaEvent_t take_event(nlse_ctx *c) {
-    if (!c->event_pool.empty()) { cudaEvent_t e = c->event_pool.back(); c->event_pool.pop_back(); return e; }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    return e;
-}
-
-struct LaunchTimer {
-    nlse_ctx *c; int kind; int64_t pts; cudaEvent_t a = nullptr;
-    LaunchTimer(nlse_ctx *c_, int kind_, int64_t pts_) : c(c_), kind(kind_), pts(pts_) {
-        if (c->timing) { a = take_event(c); cudaEventRecord(a, c->stream); }
-    }
-    ~LaunchTimer() {
-        if (c->timing) {
-            cudaEvent_t b = take_event(c);
-            cudaEventRecord(b, c->stream);
-            c->pending.push_back({kind, a, b, pts});
-        }
-    }
-};
 
 void collect_timing(nlse_ctx *c) {
     for (auto &t : c->pending) {
@@ -183,24 +46,6 @@ void collect_timing(nlse_ctx *c) {
     }
     c->pending.clear();
 }
-
-template <typename T>
-Consts<T> make_consts(const nlse_ctx *c, double kc) {
-    Consts<T> k;
-    k.ih2 = T(1.0 / (c->h * c->h));
-    k.c76 = T(7.0 / 6.0);
-    k.c112 = T(1.0 / 12.0);
-    k.c16h2 = T(1.0 / (6.0 * c->h * c->h));
-    k.a = T(c->a);
-    k.s = T(c->s);
-    k.inv_a = T(1.0 / c->a);
-    k.eps2 = sizeof(T) == 8 ? T(1e-24) : T(1e-12);
-    k.kc = T(kc);
-    return k;
-}
-
-inline unsigned blocks_for(int64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
-inline int halo_w(const nlse_ctx *c) { return c->order == NLSE_2SHOC4 ? 2 : 1; }
 
 // ------------------------------------------------------------------ TMA descriptors
 
@@ -238,24 +83,6 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
     return r == CUDA_SUCCESS;
 }
 
-// The stage kernel finishes the x-face boundary points itself (StageArgs::xfuse) when every
-// tile that owns x-face points runs the lean face-aware loop (t3_lean_ok in stage3d_tma.cuh:
-// no face point on a tile's ring, no x face on lane 0 of a tile past x = 0).
-bool xfuse_mode(const nlse_ctx *c) {
-    if (!c->tma || !c->fp || c->order != NLSE_2SHOC4) return false;
-    const char *fe = getenv("NLSE_FORCE_EDGE");
-    if (fe && fe[0] == '2') return false;
-    const char *ex = getenv("NLSE_XFUSE");
-    if (ex && ex[0] == '0') return false;
-    const int64_t nx = c->g.nx, ny = c->g.ny;
-    if ((nx - 1) % 32 == 0 || (ny - 1) % c->tma_ty == 0) return false;
-    // worth it where the light pass is bandwidth-bound on the scattered x-face points (1024^3:
-    // 2.1M of them, -0.6 % step time); on small grids the edge tiles are the critical path
-    // (87x87x203: 161 vs 150 us/step with it), so only from 2^18 x-face points on (or =1)
-    if (ex && ex[0] == '1') return true;
-    return 2 * (ny - 2) * (c->g.nz - c->g.zf_lo - c->g.zf_hi) >= (int64_t(1) << 18);
-}
-
 template <typename T, int ORDER, int TYV>
 bool build_maps(nlse_ctx *c) {
     using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
@@ -271,194 +98,24 @@ bool build_maps(nlse_ctx *c) {
     return ok;
 }
 
-// ------------------------------------------------------------------ stage launches
 
-int ybuf_of_stage(int stage) { return stage == 1 ? BUF_PSI : (stage == 3 ? BUF_OUT : BUF_TMP); }
-int obuf_of_stage(int stage) { return stage == 1 ? BUF_TMP : (stage == 2 ? BUF_OUT : (stage == 3 ? BUF_TMP : BUF_PSI)); }
-
-template <typename T, int ORDER, int BC, int STAGE, int TYV>
-void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
-    constexpr int PS = STAGE == 1 ? TMA_P1 : TMA_P;
-    using Cfg = T3Cfg<T, ORDER, PS, TYV, STAGE != 1>;
-    const int64_t nx = A.g.nx, ny = A.g.ny;
-    const int64_t mz = A.g.nz - A.g.zf_lo - A.g.zf_hi;
-    const unsigned gx = unsigned((nx + Cfg::TX - 1) / Cfg::TX);
-    const unsigned gy = unsigned((ny + Cfg::TY - 1) / Cfg::TY);
-    // z chunks: at most 128 planes (L2 locality of neighbouring tiles, r01e), and the
-    // chunk count that minimises (waves of resident CTAs) x (planes per chunk + the ~4-plane
-    // prologue), so that small grids fill the GPU in whole waves
-    const int64_t cols = int64_t(gx) * gy;
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaFuncSetAttribute(stage3d_tma<T, ORDER, BC, STAGE, PS, TYV>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage3d_tma<T, ORDER, BC, STAGE, PS, TYV>,
-                                                      Cfg::NT, Cfg::SMEM);
-        if (per_sm < 1) per_sm = 1;
+// The stage entry point of the context's (precision, dimension, order, BC) family (inst_*.cu).
+EnqueueStageFn stage_fn(const nlse_ctx *c) {
+    const bool f64 = c->prec == NLSE_FP64, shoc = c->order == NLSE_2SHOC4;
+    const int bc = c->bc == NLSE_BC_MSD ? 1 : (c->bc == NLSE_BC_L0 ? 2 : 0);
+#define NLSE_PICK(P, D, O)                                                                        \
+    if (f64 == (std::string(#P) == "f64") && c->ndim == D && shoc == (std::string(#O) == "shoc")) { \
+        const EnqueueStageFn fns[3] = {&enqueue_stage_##P##_##D##d_##O##_dirichlet,                   \
+                                       &enqueue_stage_##P##_##D##d_##O##_msd,                         \
+                                       &enqueue_stage_##P##_##D##d_##O##_l0};                         \
+        return fns[bc];                                                                           \
     }
-    static int nsm = 0;
-    if (!nsm && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) nsm = 148;
-    const int64_t resident = int64_t(nsm) * per_sm;
-    int64_t zchunk = mz, best = -1;
-    for (int64_t nzc = (mz + 127) / 128; nzc <= mz; nzc++) {
-        const int64_t ch = (mz + nzc - 1) / nzc;
-        const int64_t waves = (cols * nzc + resident - 1) / resident;
-        const int64_t cost = waves * (ch + 4);
-        if (best < 0 || cost < best) { best = cost; zchunk = ch; }
-        if (ch <= 4) break;
-    }
-    static const int64_t env_chunk = [] {
-        const char *e = getenv("NLSE_ZCHUNK");
-        return e ? std::atoll(e) : int64_t(0);
-    }();
-    if (env_chunk > 0) zchunk = env_chunk;
-    if (zchunk > mz) zchunk = mz;
-    const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
-    const int64_t items = int64_t(gx) * gy * gz;
-    // debug / measurement / tests: NLSE_FORCE_EDGE=1 runs every tile on the face-aware lean
-    // loop, =2 every tile on the per-point face path (t3_run, EDGE)
-    const char *fe = getenv("NLSE_FORCE_EDGE");
-    const int force_edge = (fe && (fe[0] == '1' || fe[0] == '2')) ? fe[0] - '0' : 0;
-    stage3d_tma<T, ORDER, BC, STAGE, PS, TYV><<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(
-        c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k, c->maps.v, A, int(zchunk), int(gx), int(gy),
-        force_edge);
+    NLSE_FAMILIES(NLSE_PICK)
+#undef NLSE_PICK
+    return nullptr;
 }
 
-template <typename T, int ORDER, int BC, int STAGE>
-void launch_tma3d(nlse_ctx *c, const StageArgs<T> &A) {
-    if (c->tma_ty == 16) launch_tma3d_ty<T, ORDER, BC, STAGE, 16>(c, A);
-    else launch_tma3d_ty<T, ORDER, BC, STAGE, 8>(c, A);
-}
-
-// One stage: interior kernel family + boundary kernel (or the generic kernel over the
-// whole owned grid).
-template <typename T, int DIM, int ORDER, int BC, int STAGE>
-void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
-    if (c->interior_kind == KK_GENERIC) {
-        LaunchTimer lt(c, KK_GENERIC, c->g.n);
-        stage_generic<T, DIM, ORDER, BC, STAGE><<<blocks_for(c->g.n, 256), 256, 0, c->stream>>>(A);
-        return;
-    }
-    // 2D/3D: the boundary kernel (disjoint outputs, same inputs: it recomputes what it needs at
-    // b') runs concurrently on a side stream, forked from and joined back into the context
-    // stream (not in timing mode, so that per-kernel shares stay attributable).  The 3D MSD
-    // light pass (c->fp: F(b') stored by the interior kernel) must follow the interior kernel.
-    const bool side = DIM >= 2 && !c->timing && c->side_stream && !c->fp;
-    if (side) {
-        const int64_t nb = n_boundary_points<DIM>(c->g);
-        cudaEventRecord(c->ev_fork, c->stream);
-        cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0);
-        stage_boundary<T, DIM, ORDER, BC, STAGE><<<blocks_for(nb, 256), 256, 0, c->side_stream>>>(A);
-        cudaEventRecord(c->ev_join, c->side_stream);
-    }
-    {
-        const int64_t ni = (c->g.nx - 2) * (DIM >= 2 ? c->g.ny - 2 : 1) *
-                           (DIM >= 3 ? c->g.nz - c->g.zf_lo - c->g.zf_hi : 1);
-        LaunchTimer lt(c, c->interior_kind, ni);
-        if (DIM == 3) {
-            if (c->interior_kind == KK_TMA3D) launch_tma3d<T, ORDER, BC, STAGE>(c, A);
-            else launch_stream3d<T, ORDER, BC, STAGE>(A, c->stream);
-        } else if (DIM == 2) {
-            launch_tile2d<T, ORDER, BC, STAGE>(A, c->stream);
-        } else {
-            launch_tile1d<T, ORDER, BC, STAGE>(A, c->stream);
-        }
-    }
-    if (side) {
-        cudaStreamWaitEvent(c->stream, c->ev_join, 0);
-    } else if (DIM == 3 && BC == BC_MSD && A.fp) {
-        // F(b') was stored by the interior kernel: a light pass after it
-        const int64_t nb = n_boundary_points<DIM>(c->g, A.xfuse != 0);
-        LaunchTimer lt(c, KK_BOUNDARY, nb);
-        stage_boundary_msd_fb<T, STAGE><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
-    } else {
-        const int64_t nb = n_boundary_points<DIM>(c->g);
-        LaunchTimer lt(c, KK_BOUNDARY, nb);
-        stage_boundary<T, DIM, ORDER, BC, STAGE><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
-    }
-}
-
-// neighbour base pointers: peer_lo[q] / peer_hi[q] address the neighbour's copy of local q
-template <typename T>
-void peer_ptrs(const nlse_ctx *c, int b, cplx<T> *&lo, cplx<T> *&hi) {
-    lo = hi = nullptr;
-    if (!c->dist || !c->connected) return;
-    const int64_t sz = c->g.sz, zg = c->g.zghost;
-    if (c->peer_alloc[b][0]) lo = (cplx<T> *)c->peer_alloc[b][0] + (zg + c->peer_nloc[0]) * sz;
-    if (c->peer_alloc[b][1]) hi = (cplx<T> *)c->peer_alloc[b][1] + (zg - c->g.nz) * sz;
-}
-
-template <typename T, int DIM, int ORDER, int BC>
-void enqueue_stage_t(nlse_ctx *c, int stage, double k, int step) {
-    using C = cplx<T>;
-    const double kc = stage == 3 ? k : (stage == 4 ? k / 6.0 : k / 2.0);
-    StageArgs<T> A{};
-    A.Y = (const C *)c->buf[ybuf_of_stage(stage)];
-    A.Psi = (const C *)c->buf[BUF_PSI];
-    A.K = (C *)c->K;
-    A.out = (C *)c->buf[obuf_of_stage(stage)];
-    A.V = (const T *)c->V;
-    A.g = c->g;
-    A.c = make_consts<T>(c, kc);
-    A.diverged = c->d_div;
-    A.step_base = c->d_steps;
-    A.step = step;
-    peer_ptrs<T>(c, obuf_of_stage(stage), A.peer_lo, A.peer_hi);
-    A.wsend = halo_w(c);
-    {
-        static const int env_hints = [] {
-            const char *e = getenv("NLSE_L2_HINTS");
-            return e ? std::atoi(e) : -1;
-        }();
-        const int64_t state_bytes = c->g.n * int64_t(4 * 2 * c->eb + (c->hasV ? c->eb : 0));
-        A.stream_hints = env_hints >= 0 ? env_hints : 0;   // r01y: evict-first hints were slower
-        (void)state_bytes;
-        static const int env_rot = [] {
-            const char *e = getenv("NLSE_RING_ROT");
-            return e ? std::atoi(e) : 1;
-        }();
-        A.ring_rot = env_rot;
-    }
-    A.fz = (C *)c->fz;
-    A.fp = (C *)c->fp;
-    A.per2 = c->per2;
-    A.xfuse = xfuse_mode(c) ? 1 : 0;
-    // (RK4_GPU) P:495-519: stages {1-3}, {4-6}, {7-9}, {10-11}
-    switch (stage) {
-        case 1: launch_stage<T, DIM, ORDER, BC, 1>(c, A); break;
-        case 2: launch_stage<T, DIM, ORDER, BC, 2>(c, A); break;
-        case 3: launch_stage<T, DIM, ORDER, BC, 3>(c, A); break;
-        default: launch_stage<T, DIM, ORDER, BC, 4>(c, A); break;
-    }
-}
-
-template <typename F>
-auto dispatch(nlse_ctx *c, F &&f) {
-    auto by_bc = [&](auto T, auto DIM, auto ORD) {
-        if (c->bc == NLSE_BC_MSD) return f(T, DIM, ORD, std::integral_constant<int, BC_MSD>());
-        if (c->bc == NLSE_BC_L0) return f(T, DIM, ORD, std::integral_constant<int, BC_L0>());
-        return f(T, DIM, ORD, std::integral_constant<int, BC_DIRICHLET>());
-    };
-    auto by_order = [&](auto T, auto DIM) {
-        if (c->order == NLSE_2SHOC4) return by_bc(T, DIM, std::integral_constant<int, ORDER_2SHOC>());
-        return by_bc(T, DIM, std::integral_constant<int, ORDER_CD>());
-    };
-    auto by_dim = [&](auto T) {
-        if (c->ndim == 1) return by_order(T, std::integral_constant<int, 1>());
-        if (c->ndim == 2) return by_order(T, std::integral_constant<int, 2>());
-        return by_order(T, std::integral_constant<int, 3>());
-    };
-    if (c->prec == NLSE_FP64) return by_dim(double());
-    return by_dim(float());
-}
-
-void enqueue_stage(nlse_ctx *c, int stage, double k, int step) {
-    dispatch(c, [&](auto T, auto DIM, auto ORD, auto BCK) {
-        enqueue_stage_t<decltype(T), decltype(DIM)::value, decltype(ORD)::value, decltype(BCK)::value>(c, stage, k,
-                                                                                                     step);
-        return 0;
-    });
-}
+void enqueue_stage(nlse_ctx *c, int stage, double k, int step) { stage_fn(c)(c, stage, k, step); }
 
 // ------------------------------------------------------------------ slab-mode plumbing
 
@@ -501,6 +158,14 @@ nlse_status enqueue_halo_refresh(nlse_ctx *c, int mode = 3) {
     return NLSE_OK;
 }
 
+// The divergence flag (first step index with a non-finite Psi, INT32_MAX = none) stays set
+// until Psi is replaced by nlse_set_psi / nlse_set_psi_device.
+nlse_status reset_divergence(nlse_ctx *c) {
+    static const int big = INT32_MAX;
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_div, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    return NLSE_OK;
+}
+
 nlse_status check_ctx(nlse_ctx *c) {
     if (!c) return fail(nullptr, NLSE_ERR_ARG, "ctx is NULL");
     if (c->sticky) return NLSE_ERR_CUDA;
@@ -531,30 +196,6 @@ void enqueue_step_stage(nlse_ctx *c, int stage, double k, int64_t n, int mode = 
 
 void enqueue_add_steps(nlse_ctx *c, int64_t n) {
     add_steps<<<1, 1, 0, c->stream>>>(c->d_steps, int(n));
-}
-
-// 1D: all nsteps in one persistent CTA when the state fits in shared memory.
-template <typename T, int ORDER, int BC>
-void launch_persist1d(nlse_ctx *c, double k, int64_t nsteps) {
-    Persist1DArgs<T> P{};
-    P.psi = (cplx<T> *)c->buf[BUF_PSI];
-    P.V = (const T *)c->V;
-    P.n = int(c->g.nx);
-    P.c[0] = make_consts<T>(c, k / 2.0);
-    P.c[1] = make_consts<T>(c, k / 2.0);
-    P.c[2] = make_consts<T>(c, k);
-    P.c[3] = make_consts<T>(c, k / 6.0);
-    P.nsteps = nsteps;
-    P.diverged = c->d_div;
-    P.step_base = c->d_steps;
-    const size_t smem = persist1d_smem<T>(P.n, c->hasV, ORDER == ORDER_2SHOC);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(rk4_1d_persistent<T, ORDER, BC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        attr = true;
-    }
-    LaunchTimer lt(c, KK_TILE1D, c->g.n * nsteps);
-    rk4_1d_persistent<T, ORDER, BC><<<1, P1_THREADS, smem, c->stream>>>(P);
 }
 
 bool use_persist1d(const nlse_ctx *c) {
@@ -597,11 +238,7 @@ bool ensure_graph(nlse_ctx *c, double k) {
 }
 
 bool graphs_enabled(const nlse_ctx *c, int64_t nsteps) {
-    static const bool env_off = [] {
-        const char *e = getenv("NLSE_GRAPHS");
-        return e && e[0] == '0';
-    }();
-    return !env_off && !c->timing && !c->virtual_group && nsteps >= 2 * GRAPH_STEPS;
+    return c->graphs && !c->timing && !c->virtual_group && nsteps >= 2 * GRAPH_STEPS;
 }
 
 nlse_status finish_steps(nlse_ctx *c, int64_t nsteps) {
@@ -829,9 +466,12 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     CREATE_TRY(cudaMallocHost(&c->h_div, sizeof(int)));
     int big = INT32_MAX;
     CREATE_TRY(cudaMemcpyAsync(c->d_div, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    c->diag_blocks = nsm * 8;
+    cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
+    c->diag_blocks = c->nsm * 8;
+    {
+        const char *e = getenv("NLSE_GRAPHS");
+        c->graphs = !(e && e[0] == '0');
+    }
     CREATE_TRY(cudaMalloc(&c->d_partial, sizeof(double) * 2 * c->diag_blocks));
     CREATE_TRY(cudaMalloc(&c->d_result, sizeof(double) * 2));
     CREATE_TRY(cudaMallocHost(&c->h_result, sizeof(double) * 2));
@@ -879,11 +519,9 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
 // graph of GRAPH_STEPS steps plus direct launches for the remainder.
 nlse_status enqueue_steps(nlse_ctx *c, double k, int64_t nsteps) {
     if (c->persist1d) {
-        dispatch(c, [&](auto T, auto DIM, auto ORD, auto BCK) {
-            if constexpr (decltype(DIM)::value == 1)
-                launch_persist1d<decltype(T), decltype(ORD)::value, decltype(BCK)::value>(c, k, nsteps);
-            return 0;
-        });
+        const bool f64 = c->prec == NLSE_FP64, shoc = c->order == NLSE_2SHOC4;
+        (f64 ? (shoc ? persist1d_f64_shoc : persist1d_f64_cd) : (shoc ? persist1d_f32_shoc : persist1d_f32_cd))(
+            c, k, nsteps);
         enqueue_add_steps(c, nsteps);
         return NLSE_OK;
     }
@@ -1061,6 +699,7 @@ nlse_status nlse_set_psi(nlse_ctx *c, const double *psi) {
     nlse_status st = check_ctx(c);
     if (st) return st;
     if (!psi) return fail(c, NLSE_ERR_ARG, "psi is NULL");
+    if ((st = reset_divergence(c))) return st;
     st = upload_complex(c, psi, c->buf[BUF_PSI]);
     c->ghost_stale = c->dist;
     return st;
@@ -1077,6 +716,7 @@ nlse_status nlse_set_psi_device(nlse_ctx *c, const void *d) {
     nlse_status st = check_ctx(c);
     if (st) return st;
     if (!d) return fail(c, NLSE_ERR_ARG, "d_psi is NULL");
+    if ((st = reset_divergence(c))) return st;
     CUDA_TRY(c, cudaMemcpyAsync(c->buf[BUF_PSI], d, size_t(c->g.n) * 2 * c->eb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->ghost_stale = c->dist;

@@ -137,14 +137,6 @@ struct T3Cfg {
     static constexpr int BOX_C_X = 2 * TX, BOX_R_X = TX, BOX_O_Y = TY;
 };
 
-// The TMA descriptors of one context: Y maps of the three halo'd buffers (Psi, Psi_tmp,
-// Psi_out; halo box), and Psi, K_tot, V over the owned box.  z coordinate of local
-// plane p is p + zghost for the halo'd buffers, p for K_tot and V.
-struct Tma3Maps {
-    CUtensorMap y[3];
-    CUtensorMap psi, k, v;
-};
-
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV, bool EDGE>
 struct T3Body {
     using C = cplx<T>;

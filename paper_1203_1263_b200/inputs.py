@@ -119,6 +119,23 @@ def random_smooth(dims, seed=SEED, modes=4, amp=1.0, offset=0.0):
 
 # ---------------------------------------------------------------- named workloads (BASELINE.json configs)
 
+def config_dims(name: str):
+    """The grid of a BASELINE configuration (as config(name)["dims"], without building its IC)."""
+    if name == "bright1d":
+        return (1025,)
+    if name.startswith("dark1d"):
+        h = float(name.split("_h")[1]) if "_h" in name else 0.1
+        return (int(round(100.0 / h)) + 1,)
+    if name == "trap2d":
+        return (1024, 1024)
+    if name in ("ring3d", "ring3d_fp32"):
+        return (87, 87, 203)
+    if name.startswith("gpe3d"):
+        n = int(name.split("_")[1]) if "_" in name else 1024
+        return (n, n, n)
+    raise KeyError(name)
+
+
 def config(name: str):
     """Return a dict describing one BASELINE.json configuration:
     dims, h, k, steps, a, s, bc, scheme, precision, psi0 (complex128), V (float64 or None)."""

@@ -5,7 +5,6 @@
     -> paper_1203_1263_b200/variants/libnlse_NAME.so ; load it with NLSE_LIB=<path>
 """
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -16,10 +15,5 @@ name, defs = sys.argv[1], sys.argv[2:]
 outdir = os.path.join(B.HERE, "variants")
 os.makedirs(outdir, exist_ok=True)
 out = os.path.join(outdir, f"libnlse_{name}.so")
-cmd = [B.NVCC, *B.NVCC_FLAGS, *defs, "-I", os.path.join(ROOT, "include"), "-o", out, *B.sources(), "-lcudart"]
-res = subprocess.run(cmd, capture_output=True, text=True)
-open(out + ".log", "w").write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-if res.returncode:
-    sys.stderr.write(res.stderr[-5000:])
-    sys.exit(1)
+B.build_to(out, defines=defs, log=out + ".log")
 print(out)

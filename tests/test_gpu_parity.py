@@ -259,6 +259,27 @@ def test_divergence_step_index_with_graphs():
     assert msgs[0] == msgs[1], msgs
 
 
+def test_divergence_flag_cleared_by_set_psi():
+    """The divergence report stays until Psi is replaced: after NLSE_ERR_DIVERGED, a fresh
+    nlse_set_psi + a stable k steps cleanly and matches the oracle."""
+    from paper_1203_1263_b200.nlse import NLSE_ERR_DIVERGED, NLSEError, Solver
+    dims = (31, 17)
+    psi = case_input(dims, seed=3)
+    k = _k(2, 0.1, "2shoc")
+    with Solver(dims, 0.1, s=-1.0, bc="dirichlet", force_dt=True) as sv:
+        sv.nlse_set_psi(psi)
+        with pytest.raises(NLSEError) as e:
+            sv.nlse_step(0.05, 400)
+        assert e.value.status == NLSE_ERR_DIVERGED
+        with pytest.raises(NLSEError):          # still non-finite: reported again
+            sv.nlse_step(k, 1)
+        sv.nlse_set_psi(psi)
+        sv.nlse_step(k, 5)
+        got = sv.nlse_get_psi()
+    ref = run_oracle(dims, 0.1, psi, k, 5, s=-1.0, bc="dirichlet")
+    assert ulp_diff(got, ref, "fp64") == 0
+
+
 def test_config5_gpe3d_full_size_sampled():
     """configs[4] at full size (1024^3 fp64 + V, 2SHOC, MSD) in the launch configuration bench.py
     times, 2 RK4 steps: sampled outputs vs the oracle, bit for bit.  A point's value after n steps
