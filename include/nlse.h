@@ -147,6 +147,13 @@ nlse_status nlse_dist_connect(nlse_ctx *ctx, const void *handles);
  * created on the same device; NLSE_ERR_ARG otherwise).  They share one stream; drive them
  * with the _group calls below. */
 nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n);
+/* Give up on a slab-mode job: set the abort flag in every rank's comm block (this rank's and
+ * the mapped peers'), so that ranks waiting at a neighbour barrier stop waiting; their next
+ * nlse_step / nlse_diagnostics returns NLSE_ERR_COMM, and so does every later call on this
+ * context.  A rank that waits longer than NLSE_BARRIER_TIMEOUT_S seconds (environment at
+ * nlse_create_dist, default 60) for a neighbour also stops and reports NLSE_ERR_COMM instead of
+ * hanging.  Safe to call while another thread is blocked in nlse_step on the same context. */
+nlse_status nlse_dist_abort(nlse_ctx *ctx);
 /* nlse_step / nlse_diagnostics over a group of contexts driven by one host thread
  * (work is enqueued interleaved per stage; mass[j], hamiltonian[j] per context, all
  * equal in slab mode). */

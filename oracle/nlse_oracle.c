@@ -12,6 +12,15 @@
 #include <stdlib.h>
 #include "nlse_oracle.h"
 
+/* Built twice: liboracle.so (serial, the reference for every test) and, with -fopenmp,
+ * liboracle_omp.so (the same sweeps split over the host cores for the all-cores CPU baseline;
+ * per-point arithmetic unchanged, so the same bits -- tests/test_oracle_pins.py checks it). */
+#ifdef _OPENMP
+#define ORC_PARFOR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_PARFOR
+#endif
+
 static int oracle_check(const oracle_problem *p)
 {
     if (!p || p->ndim < 1 || p->ndim > 3) return -1;

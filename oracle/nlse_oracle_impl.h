@@ -14,6 +14,10 @@
 #define ORC_CAT2(a, b) a##_##b
 #define ORC_CAT(a, b) ORC_CAT2(a, b)
 #define FN(name) ORC_CAT(name, SUF)
+/* ORC_PARFOR (nlse_oracle.c): "omp parallel for" on the outermost loop of each sweep when the
+ * oracle is built with -fopenmp (liboracle_omp.so, the all-cores CPU baseline of SURVEY §8(d)),
+ * nothing otherwise.  Every point's arithmetic is the same either way (the sweeps write each
+ * point once from values of the previous sweep), so both builds give the same bits. */
 
 /* Constants: evaluated in double from the user's double parameters, then
  * rounded once to REAL (reading R-CONST). */
@@ -64,11 +68,13 @@ static void FN(d_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
     const long nx = p->n[0], ny = p->n[1], nz = p->n[2];
     const long sx = 1, sy = nx, sz = nx * ny;
     if (p->ndim == 1) {
+        ORC_PARFOR
         for (long i = 1; i < nx - 1; i++) {
             REAL y2 = y[i] + y[i];
             d[i] = ((y[i - sx] + y[i + sx]) - y2) * c->ih2;
         }
     } else if (p->ndim == 2) {
+        ORC_PARFOR
         for (long j = 1; j < ny - 1; j++)
             for (long i = 1; i < nx - 1; i++) {
                 long q = j * sy + i;
@@ -76,6 +82,7 @@ static void FN(d_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
                 d[q] = (((y[q - sx] + y[q + sx]) - y2) + ((y[q - sy] + y[q + sy]) - y2)) * c->ih2;
             }
     } else {
+        ORC_PARFOR
         for (long k = 1; k < nz - 1; k++)
             for (long j = 1; j < ny - 1; j++)
                 for (long i = 1; i < nx - 1; i++) {
@@ -136,6 +143,7 @@ static void FN(d_boundary)(const oracle_problem *p, const FN(oracle_consts) *c, 
                            const REAL *yr, const REAL *yi, REAL *dr, REAL *di)
 {
     const long nx = p->n[0], ny = p->n[1], nz = p->n[2];
+    ORC_PARFOR
     for (long k = 0; k < nz; k++)
         for (long j = 0; j < ny; j++)
             for (long i = 0; i < nx; i++) {
@@ -182,10 +190,12 @@ static void FN(l_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
     const long sx = 1, sy = nx, sz = nx * ny;
     const REAL four = 4, ten = 10, twelve = 12;
     if (p->ndim == 1) {
+        ORC_PARFOR
         for (long i = 1; i < nx - 1; i++)
             l[i] = (p->order == 2) ? d[i]
                  : FN(fmar)(c->c76, d[i], -(c->c112 * (d[i - sx] + d[i + sx])));
     } else if (p->ndim == 2) {
+        ORC_PARFOR
         for (long j = 1; j < ny - 1; j++)
             for (long i = 1; i < nx - 1; i++) {
                 long q = j * sy + i;
@@ -196,6 +206,7 @@ static void FN(l_interior)(const oracle_problem *p, const FN(oracle_consts) *c,
                 l[q] = FN(fmar)(c->c16h2, cxy, -(c->c112 * td));
             }
     } else {
+        ORC_PARFOR
         for (long k = 1; k < nz - 1; k++)
             for (long j = 1; j < ny - 1; j++)
                 for (long i = 1; i < nx - 1; i++) {
@@ -244,6 +255,7 @@ static void FN(f_boundary)(const oracle_problem *p, const FN(oracle_consts) *c, 
                            const REAL *yr, const REAL *yi, REAL *fr, REAL *fi)
 {
     const long nx = p->n[0], ny = p->n[1], nz = p->n[2];
+    ORC_PARFOR
     for (long k = 0; k < nz; k++)
         for (long j = 0; j < ny; j++)
             for (long i = 0; i < nx; i++) {
@@ -266,6 +278,7 @@ static void FN(laplacian)(const oracle_problem *p, const FN(oracle_consts) *c, c
                           const REAL *yr, const REAL *yi, REAL *dr, REAL *di, REAL *lr, REAL *li)
 {
     long n = p->n[0] * p->n[1] * p->n[2];
+    ORC_PARFOR
     for (long q = 0; q < n; q++) { dr[q] = di[q] = lr[q] = li[q] = (REAL)NAN; }
     FN(d_interior)(p, c, yr, dr);
     FN(d_interior)(p, c, yi, di);
@@ -282,6 +295,7 @@ static void FN(rhs)(const oracle_problem *p, const FN(oracle_consts) *c, const R
 {
     const long nx = p->n[0], ny = p->n[1], nz = p->n[2];
     FN(laplacian)(p, c, V, yr, yi, dr, di, lr, li);
+    ORC_PARFOR
     for (long k = 0; k < nz; k++)
         for (long j = 0; j < ny; j++)
             for (long i = 0; i < nx; i++) {
@@ -338,14 +352,20 @@ int FN(oracle_step)(const oracle_problem *p, const REAL *V, REAL *re, REAL *im,
 
     for (long step = 0; step < nsteps; step++) {
         /* 1) */ FN(rhs)(p, &c, V, re, im, ktr, kti, dr, di, lr, li);
+        ORC_PARFOR
         /* 2) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k2, ktr[q], re[q]); pti[q] = FN(fmar)(k2, kti[q], im[q]); }
         /* 3) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
+        ORC_PARFOR
         /* 4) */ for (long q = 0; q < n; q++) { ktr[q] = FN(fmar)(two, kmr[q], ktr[q]); kti[q] = FN(fmar)(two, kmi[q], kti[q]); }
+        ORC_PARFOR
         /* 5) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k2, kmr[q], re[q]); pti[q] = FN(fmar)(k2, kmi[q], im[q]); }
         /* 6) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
+        ORC_PARFOR
         /* 7) */ for (long q = 0; q < n; q++) { ktr[q] = FN(fmar)(two, kmr[q], ktr[q]); kti[q] = FN(fmar)(two, kmi[q], kti[q]); }
+        ORC_PARFOR
         /* 8) */ for (long q = 0; q < n; q++) { ptr[q] = FN(fmar)(k1, kmr[q], re[q]); pti[q] = FN(fmar)(k1, kmi[q], im[q]); }
         /* 9) */ FN(rhs)(p, &c, V, ptr, pti, kmr, kmi, dr, di, lr, li);
+        ORC_PARFOR
         /* 10) */ for (long q = 0; q < n; q++) {
             re[q] = FN(fmar)(k6, ktr[q] + kmr[q], re[q]);
             im[q] = FN(fmar)(k6, kti[q] + kmi[q], im[q]);

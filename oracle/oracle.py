@@ -37,13 +37,18 @@ def library_path() -> str:
     return _LIB
 
 
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle (plain gcc, no FMA contraction, no fast-math)."""
+    """Compile the oracle (plain gcc, no FMA contraction, no fast-math): the serial library and
+    its OpenMP twin (same source, outer loops of each sweep split over threads)."""
     deps = [_SRC, os.path.join(_HERE, "nlse_oracle_impl.h"), os.path.join(_HERE, "nlse_oracle.h")]
-    if force or not os.path.exists(_LIB) or any(os.path.getmtime(d) > os.path.getmtime(_LIB) for d in deps):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *_cflags(), "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    for lib, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in deps):
+            tmp = lib + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", *_cflags(), *extra, "-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, lib)
     return _LIB
 
 
@@ -81,21 +86,22 @@ class Problem:
                         BC[self.bc], ORDER[self.scheme])
 
 
-_lib = None
+_libs = {}
 
 
-def _load():
-    global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
+def _load(omp: bool = False):
+    if omp not in _libs:
+        build()
+        lib = ctypes.CDLL(_LIB_OMP if omp else _LIB)
         for prec, T in (("f64", ctypes.c_double), ("f32", ctypes.c_float)):
             P = ctypes.POINTER(T)
-            getattr(_lib, f"oracle_step_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, ctypes.c_double, ctypes.c_long]
-            getattr(_lib, f"oracle_rhs_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, P, P]
-            getattr(_lib, f"oracle_lap_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, P, P, P, P]
+            getattr(lib, f"oracle_step_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, ctypes.c_double, ctypes.c_long]
+            getattr(lib, f"oracle_rhs_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, P, P]
+            getattr(lib, f"oracle_lap_{prec}").argtypes = [ctypes.POINTER(_Problem), P, P, P, P, P, P, P]
         D = ctypes.POINTER(ctypes.c_double)
-        _lib.oracle_diag_f64.argtypes = [ctypes.POINTER(_Problem), D, D, D, D, D]
-    return _lib
+        lib.oracle_diag_f64.argtypes = [ctypes.POINTER(_Problem), D, D, D, D, D]
+        _libs[omp] = lib
+    return _libs[omp]
 
 
 def _real_dtype(p: Problem):
@@ -134,11 +140,12 @@ def _suffix(p):
     return "f64" if p.precision == "fp64" else "f32"
 
 
-def step(p: Problem, psi, k: float, nsteps: int, V=None):
-    """nsteps RK4 steps. Returns a new complex array (complex64 for fp32)."""
+def step(p: Problem, psi, k: float, nsteps: int, V=None, omp: bool = False):
+    """nsteps RK4 steps. Returns a new complex array (complex64 for fp32).
+    omp=True runs the OpenMP build (all host cores, OMP_NUM_THREADS; same result bits)."""
     re, im = _split(p, psi)
     Vc = _v(p, V)
-    rc = getattr(_load(), f"oracle_step_{_suffix(p)}")(ctypes.byref(p.c_struct()), _ptr(Vc), _ptr(re), _ptr(im), float(k), int(nsteps))
+    rc = getattr(_load(omp), f"oracle_step_{_suffix(p)}")(ctypes.byref(p.c_struct()), _ptr(Vc), _ptr(re), _ptr(im), float(k), int(nsteps))
     if rc != 0:
         raise ValueError(f"oracle_step rejected its arguments (rc={rc})")
     return _join(re, im)

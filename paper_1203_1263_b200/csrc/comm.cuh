@@ -26,6 +26,8 @@ struct CommBlock {
     unsigned long long flags[MAX_RANKS];
     double xbuf[MAX_RANKS][2];
     unsigned long long my_epoch;   // this rank's barrier count (written by its own launches only)
+    unsigned int abort;            // nonzero: a rank gave up (nlse_dist_abort); waiters stop waiting
+    unsigned int status;           // barrier outcome of this rank: 0 ok, 1 timed out, 2 aborted
 };
 
 // Barrier arguments: signal the next epoch into sig[i]->flags[me] for every listed peer,
@@ -37,6 +39,7 @@ struct BarrierArgs {
     CommBlock *sig[MAX_RANKS];
     int wait_rank[MAX_RANKS];
     int nsig, nwait, me;
+    unsigned long long timeout_ns;   // give up waiting after this long (NLSE_BARRIER_TIMEOUT_S)
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
@@ -46,6 +49,16 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+    return t;
 }
 
 // mode bit 1: signal, bit 2: wait.  Slab mode on separate GPUs launches both in one
@@ -60,9 +73,20 @@ static __global__ void __launch_bounds__(32) peer_barrier(BarrierArgs b, int mod
         __threadfence_system();
         st_release_sys(&b.sig[t]->flags[b.me], epoch);
     }
+    // bounded wait: exponential __nanosleep backoff (64 ns .. 4 us); a set abort flag or the
+    // timeout ends it and records why in own->status (the host turns that into NLSE_ERR_COMM
+    // instead of hanging every rank on one failed or late peer)
     if ((mode & 2) && t < b.nwait) {
         const unsigned long long *f = &b.own->flags[b.wait_rank[t]];
-        while (ld_acquire_sys(f) < epoch) __nanosleep(64);
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned ns = 64;
+        while (ld_acquire_sys(f) < epoch) {
+            if (ld_relaxed_sys(&b.own->abort)) { atomicMax(&b.own->status, 2u); break; }
+            if (ld_relaxed_sys(&b.own->status)) break;   // an earlier barrier already gave up
+            if (globaltimer_ns() - t0 > b.timeout_ns) { atomicMax(&b.own->status, 1u); break; }
+            __nanosleep(ns);
+            if (ns < 4096) ns <<= 1;
+        }
     }
     __syncwarp();
 }

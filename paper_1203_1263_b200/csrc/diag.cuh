@@ -37,24 +37,26 @@ diag_partial(const cplx<T> *__restrict__ Psi, const T *__restrict__ V, Grid g, d
     __shared__ double smem[2 * (DIAG_THREADS / 32)];
     double m = 0.0, e = 0.0;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < g.n; q += stride) {
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < g.n; t += stride) {
+        // logical point t -> (i, row), element q of the (possibly pitched, g.sy >= nx) buffer
+        const int64_t row = t / g.nx, i = t - row * g.nx;
+        const int64_t q = row * g.sy + i;
         const cplx<T> p = Psi[q];
         const double pr = p.x, pi = p.y;
         const double rho = pr * pr + pi * pi;
-        const int64_t i = q % g.nx;
         double grad = 0.0;
         if (i + 1 < g.nx) {
             const cplx<T> u = Psi[q + 1];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;
         }
-        if (DIM >= 2 && ((q / g.nx) % g.ny) + 1 < g.ny) {
+        if (DIM >= 2 && (row % g.ny) + 1 < g.ny) {
             const cplx<T> u = Psi[q + g.sy];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;
         }
         // z pairs: inside the slab, or across to the upper neighbour's first plane (ghost)
-        if (DIM >= 3 && (q / g.sz) + 1 < g.nz + (g.zf_hi ? 0 : 1)) {
+        if (DIM >= 3 && (row / g.ny) + 1 < g.nz + (g.zf_hi ? 0 : 1)) {
             const cplx<T> u = Psi[q + g.sz];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;

@@ -168,12 +168,13 @@ struct PointEval {
 // One thread per grid point over the whole grid.
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
-    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= A.g.n) return;
-    const int64_t i = q % A.g.nx;
-    const int64_t j = (q / A.g.nx) % A.g.ny;
-    const int64_t k = q / A.g.sz;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= A.g.n) return;
+    const int64_t i = t % A.g.nx;
+    const int64_t j = (t / A.g.nx) % A.g.ny;
+    const int64_t k = t / (A.g.nx * A.g.ny);
     PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
+    const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_any(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
     rk_combine<STAGE, T>(A, q, k, F, psi);

@@ -61,12 +61,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 3D map over [d2][d1][d0] elements of T (d0 fastest), box {b0, b1, 1}.
-bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+// 3D map over [d2][d1][d0] elements of T (d0 fastest; rows of p0 >= d0 elements in memory),
+// box {b0, b1, 1}.  TMA needs 16-byte multiples for the row and plane strides (pitched rows,
+// nlse_ctx::pitched, make every grid qualify).
+bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t p0, uint32_t b0,
+              uint32_t b1) {
     auto enc = encode_fn();
     if (!enc) return false;
     cuuint64_t dims[3] = {d0, d1, d2};
-    cuuint64_t strides[2] = {d0 * uint64_t(eb), d0 * d1 * uint64_t(eb)};
+    cuuint64_t strides[2] = {p0 * uint64_t(eb), p0 * d1 * uint64_t(eb)};
     cuuint32_t box[3] = {b0, b1, 1}, estr[3] = {1, 1, 1};
     if (strides[0] % 16 || strides[1] % 16) return false;
     // L2 promotion of the TMA reads: NLSE_TMA_L2PROMO = 0 (none) / 64 / 128 / 256 (default) bytes
@@ -86,14 +89,14 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
 template <typename T, int ORDER, int TYV>
 bool build_maps(nlse_ctx *c) {
     using Cfg = T3Cfg<T, ORDER, TMA_P, TYV>;
-    const uint64_t nx = c->g.nx, ny = c->g.ny, nz = c->g.nz, nza = nz + 2 * c->g.zghost;
+    const uint64_t nx = c->g.nx, ny = c->g.ny, nz = c->g.nz, nza = nz + 2 * c->g.zghost, sy = c->g.sy;
     const int eb = int(sizeof(T));
     bool ok = true;
     for (int b = 0; b < 3; b++)
-        ok = ok && make_map(&c->maps.y[b], c->alloc[b], eb, 2 * nx, ny, nza, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
-    ok = ok && make_map(&c->maps.psi, c->alloc[BUF_PSI], eb, 2 * nx, ny, nza, Cfg::BOX_C_X, Cfg::BOX_O_Y);
-    ok = ok && make_map(&c->maps.k, c->K, eb, 2 * nx, ny, nz, Cfg::BOX_C_X, Cfg::BOX_O_Y);
-    if (c->V) ok = ok && make_map(&c->maps.v, c->V, eb, nx, ny, nz, Cfg::BOX_R_X, Cfg::BOX_O_Y);
+        ok = ok && make_map(&c->maps.y[b], c->alloc[b], eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
+    ok = ok && make_map(&c->maps.psi, c->alloc[BUF_PSI], eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_C_X, Cfg::BOX_O_Y);
+    ok = ok && make_map(&c->maps.k, c->K, eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_C_X, Cfg::BOX_O_Y);
+    if (c->V) ok = ok && make_map(&c->maps.v, c->V, eb, nx, ny, nz, sy, Cfg::BOX_R_X, Cfg::BOX_O_Y);
     else c->maps.v = c->maps.k;   // never dereferenced without a V array
     return ok;
 }
@@ -134,6 +137,7 @@ void enqueue_barrier(nlse_ctx *c, bool full, int mode = 3) {
         b.wait_rank[b.nwait++] = j;
     }
     if (b.nsig == 0) return;
+    b.timeout_ns = c->barrier_timeout_ns;
     LaunchTimer lt(c, KK_COMM, 0);
     peer_barrier<<<1, 32, 0, c->stream>>>(b, mode);
 }
@@ -169,6 +173,7 @@ nlse_status reset_divergence(nlse_ctx *c) {
 nlse_status check_ctx(nlse_ctx *c) {
     if (!c) return fail(nullptr, NLSE_ERR_ARG, "ctx is NULL");
     if (c->sticky) return NLSE_ERR_CUDA;
+    if (c->sticky_comm) return NLSE_ERR_COMM;
     if (c->dist && !c->connected) return fail(c, NLSE_ERR_COMM, "slab-mode context used before nlse_dist_connect");
     return NLSE_OK;
 }
@@ -241,12 +246,29 @@ bool graphs_enabled(const nlse_ctx *c, int64_t nsteps) {
     return c->graphs && !c->timing && !c->virtual_group && nsteps >= 2 * GRAPH_STEPS;
 }
 
+// Slab mode: a neighbour barrier that timed out or saw an abort (comm.cuh peer_barrier) makes
+// the context unusable (sticky NLSE_ERR_COMM): the halo data of that stage may be incomplete.
+nlse_status check_comm(nlse_ctx *c) {
+    if (!c->dist || !c->comm) return NLSE_OK;
+    unsigned st = 0;
+    CUDA_TRY(c, cudaMemcpy(&st, &c->comm->status, sizeof st, cudaMemcpyDeviceToHost));
+    if (st) {
+        c->sticky_comm = true;
+        return fail(c, NLSE_ERR_COMM, st == 2 ? "a rank aborted (nlse_dist_abort) while this rank waited at a "
+                                                 "neighbour barrier"
+                                              : "a neighbour barrier timed out (NLSE_BARRIER_TIMEOUT_S): a peer "
+                                                "rank is late, stopped or failed");
+    }
+    return NLSE_OK;
+}
+
 nlse_status finish_steps(nlse_ctx *c, int64_t nsteps) {
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(c->h_div, c->d_div, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (c->timing) collect_timing(c);
     c->steps_done += nsteps;
+    if (nlse_status st = check_comm(c)) return st;
     if (*c->h_div != INT32_MAX) {
         char buf[128];
         snprintf(buf, sizeof buf, "Psi became non-finite at step %d (0-based, counted from context creation)", *c->h_div);
@@ -294,25 +316,35 @@ nlse_status finish_diag(nlse_ctx *c, double *mass, double *ham) {
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->d_result, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (c->timing) collect_timing(c);
+    if (nlse_status st = check_comm(c)) return st;
     *mass = c->h_result[0];
     *ham = c->h_result[1];
     return NLSE_OK;
 }
 
+// Element offset of logical point q (x fastest, rows of nx points) in a buffer with rows of
+// sy >= nx elements (pitched rows, nlse_ctx::pitched).
+__device__ __forceinline__ int64_t pitched_at(int64_t q, int64_t nx, int64_t sy) {
+    if (nx == sy) return q;
+    const int64_t r = q / nx;
+    return r * sy + (q - r * nx);
+}
+// Conversions between the host layout (double, logical) and the device buffers (working
+// precision, pitched): logical points q0 .. q0 + m - 1; the logical side is indexed from q0.
 template <typename T>
-__global__ void widen_psi(const cplx<T> *src, double2 *dst, int64_t n) {
-    int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q < n) { cplx<T> v = src[q]; dst[q] = make_double2(double(v.x), double(v.y)); }
+__global__ void widen_psi(const cplx<T> *src, double2 *dst, int64_t q0, int64_t m, int64_t nx, int64_t sy) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < m) { cplx<T> v = src[pitched_at(q0 + t, nx, sy)]; dst[t] = make_double2(double(v.x), double(v.y)); }
 }
 template <typename T>
-__global__ void narrow_psi(const double2 *src, cplx<T> *dst, int64_t n) {
-    int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q < n) { double2 v = src[q]; cplx<T> r; r.x = T(v.x); r.y = T(v.y); dst[q] = r; }
+__global__ void narrow_psi(const double2 *src, cplx<T> *dst, int64_t q0, int64_t m, int64_t nx, int64_t sy) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < m) { double2 v = src[t]; cplx<T> r; r.x = T(v.x); r.y = T(v.y); dst[pitched_at(q0 + t, nx, sy)] = r; }
 }
 template <typename T>
-__global__ void narrow_real(const double *src, T *dst, int64_t n) {
-    int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q < n) dst[q] = T(src[q]);
+__global__ void narrow_real(const double *src, T *dst, int64_t m, int64_t nx, int64_t sy) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < m) dst[pitched_at(t, nx, sy)] = T(src[t]);
 }
 
 double linear_bound(int ndim, double a, double h, nlse_order order) {
@@ -323,16 +355,17 @@ double linear_bound(int ndim, double a, double h, nlse_order order) {
 // Host double (re, im) -> device working precision, staged through Psi_out (scratch
 // between calls) for fp32.
 nlse_status upload_complex(nlse_ctx *c, const double *host, void *dev) {
-    const size_t n = size_t(c->g.n);
+    const size_t n = size_t(c->g.n), nx = size_t(c->g.nx), sy = size_t(c->g.sy);
     if (c->prec == NLSE_FP64) {
-        CUDA_TRY(c, cudaMemcpyAsync(dev, host, n * 16, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(c, cudaMemcpy2DAsync(dev, sy * 16, host, nx * 16, nx * 16, n / nx, cudaMemcpyHostToDevice, c->stream));
     } else {
-        const size_t chunk = n / 2 > 0 ? n / 2 : 1;  // outb holds n float2 = n/2 double2
+        const size_t chunk = n / 2 > 0 ? n / 2 : 1;  // outb holds >= n float2 = n/2 double2
         double2 *scratch = (double2 *)c->buf[BUF_OUT];
         for (size_t off = 0; off < n; off += chunk) {
             size_t m = std::min(chunk, n - off);
             CUDA_TRY(c, cudaMemcpyAsync(scratch, host + 2 * off, m * 16, cudaMemcpyHostToDevice, c->stream));
-            narrow_psi<float><<<blocks_for(m, 256), 256, 0, c->stream>>>(scratch, (float2 *)dev + off, int64_t(m));
+            narrow_psi<float><<<blocks_for(m, 256), 256, 0, c->stream>>>(scratch, (float2 *)dev, int64_t(off),
+                                                                          int64_t(m), int64_t(nx), int64_t(sy));
             CUDA_TRY(c, cudaGetLastError());
         }
     }
@@ -341,15 +374,16 @@ nlse_status upload_complex(nlse_ctx *c, const double *host, void *dev) {
 }
 
 nlse_status download_complex(nlse_ctx *c, const void *dev, double *host) {
-    const size_t n = size_t(c->g.n);
+    const size_t n = size_t(c->g.n), nx = size_t(c->g.nx), sy = size_t(c->g.sy);
     if (c->prec == NLSE_FP64) {
-        CUDA_TRY(c, cudaMemcpyAsync(host, dev, n * 16, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaMemcpy2DAsync(host, nx * 16, dev, sy * 16, nx * 16, n / nx, cudaMemcpyDeviceToHost, c->stream));
     } else {
         const size_t chunk = n / 2 > 0 ? n / 2 : 1;
         double2 *scratch = (double2 *)c->buf[BUF_OUT];
         for (size_t off = 0; off < n; off += chunk) {
             size_t m = std::min(chunk, n - off);
-            widen_psi<float><<<blocks_for(m, 256), 256, 0, c->stream>>>((const float2 *)dev + off, scratch, int64_t(m));
+            widen_psi<float><<<blocks_for(m, 256), 256, 0, c->stream>>>((const float2 *)dev, scratch, int64_t(off),
+                                                                         int64_t(m), int64_t(nx), int64_t(sy));
             CUDA_TRY(c, cudaGetLastError());
             CUDA_TRY(c, cudaMemcpyAsync(host + 2 * off, scratch, m * 16, cudaMemcpyDeviceToHost, c->stream));
         }
@@ -407,10 +441,23 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->dist = dist; c->rank = rank; c->nranks = nranks; c->z0 = z0;
     c->g.nx = dims[0]; c->g.ny = dims[1]; c->g.nz = nloc;
     c->g.sy = dims[0]; c->g.sz = dims[0] * dims[1]; c->g.n = n;
+    c->eb = prec == NLSE_FP64 ? 8 : 4;
+    // Pitched rows: the 3D TMA kernels need 16-byte row strides in every array (complex rows
+    // 2*nx*eb, V rows nx*eb bytes); the paper pads rows the same way (cudaMallocPitch).
+    // Rows are padded to sy points only where they would not qualify (e.g. fp32 with odd nx:
+    // the paper's 87x87x203 ring); padding is zero, never read (TMA boxes stop at nx) or written.
+    if (ndim == 3 && !(flags & NLSE_FLAG_GENERIC_KERNELS) && std::string(env_kernel()) != "v1") {
+        const int64_t per16 = 16 / c->eb;                       // points per 16 bytes of a real row
+        const bool bad = (2 * dims[0] * c->eb) % 16 != 0 || (V && (dims[0] * c->eb) % 16 != 0);
+        if (bad) {
+            c->g.sy = (dims[0] + per16 - 1) / per16 * per16;
+            c->g.sz = c->g.sy * dims[1];
+            c->pitched = true;
+        }
+    }
     c->g.zf_lo = (!dist || rank == 0) ? 1 : 0;
     c->g.zf_hi = (!dist || rank == nranks - 1) ? 1 : 0;
     c->g.zghost = dist ? w : 0;
-    c->eb = prec == NLSE_FP64 ? 8 : 4;
     c->hasV = V != nullptr;
     cudaGetDevice(&c->device);
     if (flags & NLSE_FLAG_GENERIC_KERNELS) c->interior_kind = KK_GENERIC;
@@ -436,23 +483,29 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         CREATE_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
     const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.sz) * cb;
-    const size_t halo_bytes = size_t(n) * cb + 2 * size_t(c->g.zghost) * plane;
+    const size_t halo_bytes = (size_t(nloc) + 2 * size_t(c->g.zghost)) * plane;
+    const size_t cells = size_t(nloc) * size_t(c->g.sz);    // allocated points (>= n with pitched rows)
     for (int b = 0; b < 3; b++) {
         CREATE_TRY(cudaMalloc(&c->alloc[b], halo_bytes));
         CREATE_TRY(cudaMemsetAsync(c->alloc[b], 0, halo_bytes, c->stream));
         c->buf[b] = (char *)c->alloc[b] + size_t(c->g.zghost) * plane;
     }
-    CREATE_TRY(cudaMalloc(&c->K, size_t(n) * cb));
-    c->device_bytes = int64_t(3 * halo_bytes + size_t(n) * cb);
+    CREATE_TRY(cudaMalloc(&c->K, cells * cb));
+    CREATE_TRY(cudaMemsetAsync(c->K, 0, cells * cb, c->stream));
+    c->device_bytes = int64_t(3 * halo_bytes + cells * cb);
     if (V) {
-        CREATE_TRY(cudaMalloc(&c->V, size_t(n) * c->eb));
-        c->device_bytes += int64_t(size_t(n) * c->eb);
+        CREATE_TRY(cudaMalloc(&c->V, cells * c->eb));
+        CREATE_TRY(cudaMemsetAsync(c->V, 0, cells * c->eb, c->stream));
+        c->device_bytes += int64_t(cells * c->eb);
+        const size_t nx = size_t(c->g.nx), sy = size_t(c->g.sy);
         if (prec == NLSE_FP64) {
-            CREATE_TRY(cudaMemcpyAsync(c->V, V, size_t(n) * 8, cudaMemcpyHostToDevice, c->stream));
+            CREATE_TRY(cudaMemcpy2DAsync(c->V, sy * 8, V, nx * 8, nx * 8, size_t(n) / nx, cudaMemcpyHostToDevice,
+                                         c->stream));
         } else {
-            // stage the double V through K (n complex floats = n doubles) and round once on the device
+            // stage the double V through K (>= n complex floats = n doubles) and round once on the device
             CREATE_TRY(cudaMemcpyAsync(c->K, V, size_t(n) * 8, cudaMemcpyHostToDevice, c->stream));
-            narrow_real<float><<<blocks_for(n, 256), 256, 0, c->stream>>>((const double *)c->K, (float *)c->V, n);
+            narrow_real<float><<<blocks_for(n, 256), 256, 0, c->stream>>>((const double *)c->K, (float *)c->V, n,
+                                                                           int64_t(nx), int64_t(sy));
             CREATE_TRY(cudaGetLastError());
         }
     }
@@ -471,6 +524,9 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     {
         const char *e = getenv("NLSE_GRAPHS");
         c->graphs = !(e && e[0] == '0');
+        const char *t = getenv("NLSE_BARRIER_TIMEOUT_S");
+        const double ts = t ? std::atof(t) : 60.0;
+        c->barrier_timeout_ns = ts > 0 ? (unsigned long long)(ts * 1e9) : 60000000000ull;
     }
     CREATE_TRY(cudaMalloc(&c->d_partial, sizeof(double) * 2 * c->diag_blocks));
     CREATE_TRY(cudaMalloc(&c->d_result, sizeof(double) * 2));
@@ -480,7 +536,11 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         const std::string ek = env_kernel();
         bool ok = ek != "v1";
         const char *ety = getenv("NLSE_TMA_TY");
-        c->tma_ty = (ety && std::atoi(ety) == 8) ? 8 : 16;   // 16 measured faster (r01f, r01j)
+        // fp64: 16-row tiles (512 threads, 1 CTA/SM, <= 128 registers) measured faster (r01f, r01j);
+        // fp32: 8-row tiles (256 threads, 3 CTAs/SM, 80 registers, spill-free) measured faster than
+        // 16 rows at 1 CTA/SM (no spills) or 2 CTAs/SM (64 registers, spills): r02b
+        const int ty_default = prec == NLSE_FP32 ? 8 : 16;
+        c->tma_ty = ety ? (std::atoi(ety) == 8 ? 8 : 16) : ty_default;
         if (ok) {
             auto bm = [&](auto TYc) {
                 constexpr int TYV = decltype(TYc)::value;
@@ -695,6 +755,26 @@ nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n) {
     return NLSE_OK;
 }
 
+nlse_status nlse_dist_abort(nlse_ctx *c) {
+    if (!c) return fail(nullptr, NLSE_ERR_ARG, "ctx is NULL");
+    if (!c->dist || !c->comm) return fail(c, NLSE_ERR_ARG, "not a slab-mode context");
+    // on a separate stream: the context stream may be blocked behind a waiting barrier kernel
+    cudaStream_t s = nullptr;
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    static const unsigned one = 1;
+    cudaError_t e = cudaSuccess;
+    for (int j = 0; j < c->nranks && e == cudaSuccess; j++) {
+        CommBlock *cb = j == c->rank ? c->comm : c->peer_comm[j];
+        if (cb) e = cudaMemcpyAsync(&cb->abort, &one, sizeof one, cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return fail(c, NLSE_ERR_CUDA, std::string("nlse_dist_abort: ") + cudaGetErrorString(e));
+    c->sticky_comm = true;
+    c->err = "aborted by nlse_dist_abort";
+    return NLSE_OK;
+}
+
 nlse_status nlse_set_psi(nlse_ctx *c, const double *psi) {
     nlse_status st = check_ctx(c);
     if (st) return st;
@@ -717,7 +797,9 @@ nlse_status nlse_set_psi_device(nlse_ctx *c, const void *d) {
     if (st) return st;
     if (!d) return fail(c, NLSE_ERR_ARG, "d_psi is NULL");
     if ((st = reset_divergence(c))) return st;
-    CUDA_TRY(c, cudaMemcpyAsync(c->buf[BUF_PSI], d, size_t(c->g.n) * 2 * c->eb, cudaMemcpyDeviceToDevice, c->stream));
+    const size_t row = size_t(c->g.nx) * 2 * c->eb;
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->buf[BUF_PSI], size_t(c->g.sy) * 2 * c->eb, d, row, row, size_t(c->g.n / c->g.nx),
+                                  cudaMemcpyDeviceToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->ghost_stale = c->dist;
     return NLSE_OK;
@@ -727,7 +809,9 @@ nlse_status nlse_get_psi_device(nlse_ctx *c, void *d) {
     nlse_status st = check_ctx(c);
     if (st) return st;
     if (!d) return fail(c, NLSE_ERR_ARG, "d_psi is NULL");
-    CUDA_TRY(c, cudaMemcpyAsync(d, c->buf[BUF_PSI], size_t(c->g.n) * 2 * c->eb, cudaMemcpyDeviceToDevice, c->stream));
+    const size_t row = size_t(c->g.nx) * 2 * c->eb;
+    CUDA_TRY(c, cudaMemcpy2DAsync(d, row, c->buf[BUF_PSI], size_t(c->g.sy) * 2 * c->eb, row, size_t(c->g.n / c->g.nx),
+                                  cudaMemcpyDeviceToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return NLSE_OK;
 }
@@ -767,10 +851,12 @@ nlse_status nlse_run_frames(nlse_ctx *c, double k, int64_t chunk, int nframes, d
         if (f >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
         double2 *snap = (double2 *)c->snap[b];
         if (c->prec == NLSE_FP64) {
-            CUDA_TRY(c, cudaMemcpyAsync(snap, c->buf[BUF_PSI], fb, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_TRY(c, cudaMemcpy2DAsync(snap, size_t(c->g.nx) * 16, c->buf[BUF_PSI], size_t(c->g.sy) * 16,
+                                          size_t(c->g.nx) * 16, n / size_t(c->g.nx), cudaMemcpyDeviceToDevice,
+                                          c->stream));
         } else {
-            widen_psi<float><<<blocks_for(int64_t(n), 256), 256, 0, c->stream>>>((const float2 *)c->buf[BUF_PSI],
-                                                                                snap, int64_t(n));
+            widen_psi<float><<<blocks_for(int64_t(n), 256), 256, 0, c->stream>>>(
+                (const float2 *)c->buf[BUF_PSI], snap, 0, int64_t(n), c->g.nx, c->g.sy);
             CUDA_TRY(c, cudaGetLastError());
         }
         CUDA_TRY(c, cudaEventRecord(c->ev_snap[b], c->stream));

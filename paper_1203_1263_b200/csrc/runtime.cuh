@@ -79,6 +79,8 @@ struct nlse_ctx {
     int64_t device_bytes = 0;
     std::string err;
     bool sticky = false;
+    bool sticky_comm = false;        // slab mode: a barrier timed out / was aborted (NLSE_ERR_COMM)
+    unsigned long long barrier_timeout_ns = 60000000000ull;
     bool timing = false;
     std::vector<TimedLaunch> pending;
     std::vector<cudaEvent_t> event_pool;

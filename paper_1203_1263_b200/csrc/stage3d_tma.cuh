@@ -972,8 +972,18 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
 // consecutive tiles of one z chunk (their shared halo rows and columns are L2 hits).
 // Measured alternatives (r01g-j: a persistent grid drawing items from a counter, banded
 // tile orders) were not faster.
+// Resident CTAs per SM the register allocation is sized for (__launch_bounds__): fp64 TY=16 one
+// CTA (<= 128 registers); fp32 TY=16 NLSE_F32_MINB CTAs (2: <= 64 registers, which spills the
+// 2SHOC loop; 1: <= 128 registers, no spills, half the resident warps).
+#ifndef NLSE_F32_MINB
+#define NLSE_F32_MINB 1
+#endif
+template <typename T, int TYV>
+constexpr int t3_min_blocks() {
+    return TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : NLSE_F32_MINB);
+}
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
-__global__ void __launch_bounds__(32 * TYV, (TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : 2)))
+__global__ void __launch_bounds__(32 * TYV, t3_min_blocks<T, TYV>())
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
             const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge) {

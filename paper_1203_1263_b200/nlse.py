@@ -91,6 +91,7 @@ def _load():
     lib.nlse_dist_export.argtypes = [P, ctypes.c_char_p]
     lib.nlse_dist_connect.argtypes = [P, ctypes.c_char_p]
     lib.nlse_dist_connect_local.argtypes = [ctypes.POINTER(P), ctypes.c_int]
+    lib.nlse_dist_abort.argtypes = [P]
     lib.nlse_step_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_double, ctypes.c_int64]
     lib.nlse_run_frames.argtypes = [P, ctypes.c_double, ctypes.c_int64, ctypes.c_int, D]
     lib.nlse_diagnostics_group.argtypes = [ctypes.POINTER(P), ctypes.c_int, D, D]
@@ -98,7 +99,7 @@ def _load():
               "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_get_stream", "nlse_set_timing",
               "nlse_get_timing", "nlse_reset_timing", "nlse_get_info", "nlse_slab_range", "nlse_create_dist",
               "nlse_dist_export", "nlse_dist_connect", "nlse_dist_connect_local", "nlse_step_group",
-              "nlse_diagnostics_group", "nlse_run_frames"):
+              "nlse_diagnostics_group", "nlse_run_frames", "nlse_dist_abort"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -110,7 +111,8 @@ EXPORTS = ("nlse_create", "nlse_set_psi", "nlse_get_psi", "nlse_set_psi_device",
            "nlse_step", "nlse_diagnostics", "nlse_stability_bound", "nlse_last_error", "nlse_status_string",
            "nlse_destroy", "nlse_get_stream", "nlse_set_timing", "nlse_get_timing", "nlse_reset_timing",
            "nlse_get_info", "nlse_slab_range", "nlse_create_dist", "nlse_dist_export", "nlse_dist_connect",
-           "nlse_dist_connect_local", "nlse_step_group", "nlse_diagnostics_group", "nlse_run_frames")
+           "nlse_dist_connect_local", "nlse_step_group", "nlse_diagnostics_group", "nlse_run_frames",
+           "nlse_dist_abort")
 
 
 def _check(st, ctx=None):
@@ -251,6 +253,9 @@ class Solver:
         """handles: the nranks exported handles in rank order (list of bytes or one bytes object)."""
         blob = b"".join(handles) if not isinstance(handles, (bytes, bytearray)) else bytes(handles)
         _check(lib.nlse_dist_connect(self.ctx, blob), self.ctx)
+
+    def nlse_dist_abort(self):
+        _check(lib.nlse_dist_abort(self.ctx), self.ctx)
 
     # --- conveniences ----------------------------------------------------------------------------
     set_psi = nlse_set_psi

@@ -93,3 +93,43 @@ def assert_parity(gpu, ref, precision, bitwise=True, what=""):
 def case_input(dims, seed, kind="smooth"):
     """Seeded input with a background of modulus ~1 (MSD needs |Psi_b| away from 0)."""
     return inputs.random_smooth(tuple(dims), seed=seed, modes=5, amp=0.4, offset=1.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# MSD division guard (DESIGN.md reading R-MSD-GUARD): inputs whose inward neighbours b' are zero
+# or sit just below / above the threshold |Y_b'|^2 = eps^2, so the guarded branch is taken
+# ---------------------------------------------------------------------------------------------
+
+EPS = {"fp64": 1e-12, "fp32": 1e-6}
+
+
+def guard_points(dims):
+    """(zero, below, above): lists of grid indices (x, y, z order, as many as ndim) of points
+    one step in from the boundary: `zero` get Psi = 0, `below` |Psi| = eps/2 (guarded),
+    `above` |Psi| = 2 eps (not guarded).  They cover face, edge and corner neighbours b'."""
+    n = list(dims)
+    d = len(n)
+    if d == 1:
+        return [(1,)], [(n[0] - 2,)], []
+    if d == 2:
+        return ([(1, 5), (1, 1), (10, 1), (n[0] - 2, n[1] - 2), (n[0] - 2, 9)],
+                [(1, 12)], [(1, 14), (7, n[1] - 2)])
+    return ([(1, 5, 7), (1, 1, 9), (1, 1, 1), (10, 1, 4), (12, 8, 1), (n[0] - 2, n[1] - 2, n[2] - 2),
+             (20, n[1] - 2, 11), (n[0] - 2, 10, 13), (33, 9, n[2] - 2)],
+            [(1, 16, 6), (40, 1, 6)], [(1, 14, 6), (n[0] - 2, 6, 8)])
+
+
+def guard_field(dims, precision, seed=1203, above=True):
+    """A smooth field of modulus ~1 with the guard_points set (phase kept).  above=False leaves
+    out the unguarded near-threshold points: there F_b = i Im(F_b'/Y_b') Y_b is ~1e12 times the
+    field, which a time integration cannot survive (single-evaluation pins only)."""
+    psi = case_input(dims, seed=seed)
+    zero, below, above_pts = guard_points(dims)
+    above = above_pts if above else []
+    eps = EPS[precision]
+    for pts, mag in ((zero, 0.0), (below, 0.5 * eps), (above, 2.0 * eps)):
+        for p in pts:
+            idx = tuple(reversed(p))
+            v = psi[idx]
+            psi[idx] = 0.0 if mag == 0.0 else mag * v / abs(v)
+    return psi

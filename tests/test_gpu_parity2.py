@@ -1,0 +1,120 @@
+"""GPU parity, round 2: the configurations the round-1 review found without a GPU-vs-oracle
+check -- the MSD division guard taken on every kernel path, 1D grids above the persistent-CTA
+limit, the frames model against oracle frames, and the BASELINE configurations after their full
+stated step counts (against oracle digests in tests/golden/oracle_sha256.json).
+Bar: bit-identical, as test_gpu_parity.py."""
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from helpers import assert_parity, case_input, guard_field, run_gpu, run_oracle
+from paper_1203_1263_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "oracle_sha256.json")
+
+
+def _k(ndim, h, scheme):
+    kb = h * h / (ndim * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
+    return 0.5 * kb
+
+
+VARIANT_ENV = {
+    "fast": {}, "generic": {},
+    "edge_lean": {"NLSE_FORCE_EDGE": "1"}, "edge_pp": {"NLSE_FORCE_EDGE": "2"},
+    "msd_recompute": {"NLSE_MSD_FB": "0"}, "xfuse_off": {"NLSE_XFUSE": "0"}, "xfuse_on": {"NLSE_XFUSE": "1"},
+    "v1": {"NLSE_3D_KERNEL": "v1"},
+}
+
+
+@pytest.mark.parametrize("kernel", list(VARIANT_ENV))
+@pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("dims", [(1029,), (6001,), (133, 70), (70, 37, 29)], ids=["1d", "1d_tiled", "2d", "3d"])
+def test_msd_eps_guard_bitwise(dims, precision, withV, kernel, monkeypatch):
+    """R-MSD-GUARD on the GPU: Psi_b' = 0 and eps/2 (guard taken) at face, edge and corner
+    neighbours (tests/helpers.guard_points); every kernel path that forms an MSD
+    boundary value (the TMA stage kernel's face D and x-face F, the light pass, the recompute
+    kernel, the 2D tile kernel, the 1D persistent and tiled kernels, the generic kernel) matches
+    the oracle bit for bit.  The guard fires in stage 1 of step 1; later stages see the evolved
+    field."""
+    if kernel not in ("fast", "generic") and len(dims) != 3:
+        pytest.skip("3D kernel variant")
+    for k_, v_ in VARIANT_ENV[kernel].items():
+        monkeypatch.setenv(k_, v_)
+    ndim = len(dims)
+    h = {1: 0.05, 2: 0.2, 3: 0.5}[ndim]
+    psi0 = guard_field(dims, precision, above=False)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=300 + ndim)) if withV else None
+    kw = dict(a=0.9, s=-1.1, V=V, bc="msd", scheme="2shoc", precision=precision)
+    k = _k(ndim, h, "2shoc")
+    ref = run_oracle(dims, h, psi0, k, 3, **kw)
+    assert np.all(np.isfinite(ref))
+    got = run_gpu(dims, h, psi0, k, 3, generic=kernel == "generic", **kw)
+    assert_parity(got, ref, precision, what=f"guard {dims} {precision} V={withV} {kernel}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("n", [6001, 100001])
+def test_1d_large_grids_bitwise(n, scheme, bc, precision):
+    """1D grids above the persistent single-CTA limit (the paper's Table 1 runs 1D to 3e6 points,
+    P:664-686) take the tiled 1D stage kernels: bit for bit against the oracle, with a V array."""
+    dims = (n,)
+    h = 0.05
+    psi0 = case_input(dims, seed=n % 997)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=11))
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    k = _k(1, h, scheme)
+    ref = run_oracle(dims, h, psi0, k, 9, **kw)
+    got, info = run_gpu(dims, h, psi0, k, 9, with_info=True, **kw)
+    assert info["variant"] != "rk4_1d_persistent", info
+    assert_parity(got, ref, precision, what=f"1D n={n} {scheme} {bc} {precision} {info['variant']}")
+
+
+@pytest.mark.parametrize("ndim,precision,chunk", [(3, "fp64", 20), (3, "fp32", 3), (1, "fp64", 7), (2, "fp32", 5),
+                                                  (2, "fp64", 17)])
+def test_run_frames_match_oracle(ndim, precision, chunk):
+    """nlse_run_frames (the paper's frames model): frame f equals the oracle's
+    field after (f + 1) x chunk steps, bit for bit."""
+    from paper_1203_1263_b200.nlse import Solver
+    dims = {1: (301,), 2: (70, 41), 3: (40, 26, 22)}[ndim]
+    h = {1: 0.1, 2: 0.2, 3: 0.5}[ndim]
+    psi0 = case_input(dims, seed=91)
+    V = 0.2 * np.abs(inputs.random_smooth(dims, seed=92))
+    k = _k(ndim, h, "2shoc")
+    kw = dict(s=-1.0, V=V, bc="msd", scheme="2shoc", precision=precision)
+    with Solver(dims, h, force_dt=True, **kw) as sv:
+        sv.nlse_set_psi(psi0)
+        frames = sv.nlse_run_frames(k, chunk, 3)
+    ref = psi0
+    for f in range(3):
+        ref = run_oracle(dims, h, ref, k, chunk, **kw)
+        assert_parity(frames[f], ref, precision, what=f"frame {f}")
+
+
+def _golden(name):
+    with open(GOLDEN) as fh:
+        return json.load(fh)[name]
+
+
+@pytest.mark.parametrize("name", ["trap2d_fp64_1000", "ring3d_fp64_3360", "ring3d_fp32_3360"])
+def test_full_step_counts_match_oracle_digest(name):
+    """BASELINE configs[2] (1024^2 trap, 1000 steps) and configs[3] (87x87x203 ring, 3360 steps,
+    P:69) after their stated step counts: the SHA-256 of the whole GPU field equals the digest of
+    the oracle's field (scripts/make_goldens.py, which calls only oracle/)."""
+    g = _golden(name)
+    cfg = inputs.config(g["config"])
+    assert list(cfg["dims"]) == g["dims"] and cfg["k"] == g["k"]
+    got = run_gpu(cfg["dims"], cfg["h"], cfg["psi0"], cfg["k"], g["steps"], a=cfg["a"], s=cfg["s"], V=cfg["V"],
+                  bc=cfg["bc"], scheme=cfg["scheme"], precision=g["precision"], force_dt=False)
+    dt = np.complex128 if g["precision"] == "fp64" else np.complex64
+    h = hashlib.sha256(np.ascontiguousarray(got.astype(dt)).tobytes()).hexdigest()
+    assert np.all(np.isfinite(got)) and g["finite"]
+    assert h == g["sha256"], (name, float(np.abs(got).max()), g["max_abs"])

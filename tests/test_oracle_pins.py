@@ -505,3 +505,85 @@ def test_l0_bc_forms_consistent(oracle_lib, precision):
         [-1 if a == ax else 1 for a in range(3)]) for ax, n in enumerate(reversed(dims)))
     assert np.all(D[nb == 1] == 0)
     assert np.all(np.isnan(D[nb >= 2]))
+
+
+# ---------------------------------------------------------------------------------------------
+# MSD division guard, reading R-MSD-GUARD (the paper is silent on 1/Psi_b' at a zero)
+# ---------------------------------------------------------------------------------------------
+
+def _boundary_points(dims):
+    """All boundary points (x, y, z order) with their diagonal inward neighbour b' (R-MSD-NBR)
+    and, for face points, the normal inward neighbour (R-DFACE)."""
+    out = []
+    for q in np.ndindex(*dims):
+        bnd = [i == 0 or i == n - 1 for i, n in zip(q, dims)]
+        if not any(bnd):
+            continue
+        diag = tuple(min(max(i, 1), n - 2) for i, n in zip(q, dims))
+        normal = diag if sum(bnd) == 1 else None
+        out.append((q, diag, normal))
+    return out
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_msd_eps_guard(oracle_lib, ndim, precision):
+    """Where |Y_b'|^2 < eps^2 (eps^2 = 1e-24 fp64, 1e-12 fp32) the MSD quotient is taken as 0:
+    F_b = 0 exactly ((msd) P:331-335) and D_b = ((N_b' - N_b)/a) Y_b ((BCMSDlap) P:336-344 without
+    the Re(D_b'/Y_b') term).  Inputs put Psi_b' = 0, eps/2 (guarded) and 2 eps (not guarded) at
+    face, edge and corner neighbours; every other boundary point must keep its quotient (F_b != 0,
+    D_b != the guarded form), and unguarded points near the threshold follow (msd) exactly."""
+    from helpers import EPS, guard_field, guard_points
+    dims = {1: (41,), 2: (30, 23), 3: (44, 21, 17)}[ndim]
+    T = np.float64 if precision == "fp64" else np.float32
+    psi = guard_field(dims, precision)
+    p = Problem(dims, 0.5, a=0.75, s=-1.3, bc="msd", scheme="2shoc", precision=precision)
+    F = oracle.rhs(p, psi)
+    D, _ = oracle.laplacian(p, psi)
+    Y = psi.astype(np.complex128 if precision == "fp64" else np.complex64)
+    yr, yi = Y.real.astype(T), Y.imag.astype(T)
+    rho = yr * yr + yi * yi
+    eps2 = T(EPS[precision] ** 2)
+    a, s = T(0.75), T(-1.3)
+    inv_a = T(1.0 / 0.75)
+    at = lambda arr, q: arr[tuple(reversed(q))]
+    zero, below, above = guard_points(dims)
+    n_guard = n_quot = 0
+    for b, bd, bn in _boundary_points(dims):
+        fb = at(F, b)
+        if at(rho, bd) < eps2:
+            n_guard += 1
+            assert fb.real == 0 and fb.imag == 0, (b, bd, fb)
+        else:
+            n_quot += 1
+            f1 = at(F, bd)
+            m = (T(f1.imag) * at(yr, bd) - T(f1.real) * at(yi, bd)) / at(rho, bd)
+            assert fb.real == -(m * at(yi, b)) and fb.imag == m * at(yr, b), (b, fb)
+            assert fb != 0, b
+        if bn is not None:
+            nb, n1 = s * at(rho, b), s * at(rho, bn)
+            g = (n1 - nb) * inv_a
+            guarded = (g * at(yr, b), g * at(yi, b))
+            db = at(D, b)
+            if at(rho, bn) < eps2:
+                assert (db.real, db.imag) == guarded, (b, db, guarded)
+            else:
+                assert (db.real, db.imag) != guarded, b
+    # every planted point is an inward neighbour of some boundary point and fired (or not) as set
+    assert all(at(rho, q) == 0 for q in zero) and all(at(rho, q) < eps2 for q in below)
+    assert all(at(rho, q) > eps2 for q in above)
+    assert n_guard >= len(zero) + len(below) and (n_quot > 0 or ndim == 1)
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+def test_openmp_build_gives_the_same_bits(oracle_lib, bc):
+    """The all-cores build (liboracle_omp.so, bench.py's cpu_baseline) splits only the outer loop
+    of each sweep over threads: its result equals the serial oracle bit for bit."""
+    dims = (23, 19, 17)
+    psi = case_field(dims, seed=7)
+    V = np.abs(case_field(dims, seed=8)) * 0.2
+    for prec in ("fp64", "fp32"):
+        p = Problem(dims, 0.5, a=0.9, s=-1.1, bc=bc, scheme="2shoc", precision=prec)
+        a = oracle.step(p, psi, 0.01, 4, V)
+        b = oracle.step(p, psi, 0.01, 4, V, omp=True)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (bc, prec)
