@@ -333,7 +333,16 @@ def main():
     td = timing[dom]
     avg_launch_ms = td["ms"] / max(td["launches"], 1)
     pts_per_launch = td["points"] / max(td["launches"], 1)
-    alg_bytes_launch = pts_per_launch * B / 4.0          # B_min per point per step spread over 4 stages
+    if dom == "fused3d_cd":
+        # temporal blocking (§8(f) rank 2): each launch is two stages; its compulsory bytes are
+        # (3c + r_V) for S1+S2 and (4c + r_V) for S3+S4, i.e. (7c + 2 r_V)/2 per point on average
+        c_ = 16 if cfg["precision"] == "fp64" else 8
+        r_ = (c_ // 2) if cfg["V"] is not None else 0
+        B_fused = 7 * c_ + 2 * r_
+        alg_bytes_launch = pts_per_launch * B_fused / 2.0
+    else:
+        B_fused = None
+        alg_bytes_launch = pts_per_launch * B / 4.0      # B_min per point per step spread over 4 stages
     achieved = alg_bytes_launch / (avg_launch_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(dom, pts_per_launch)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -343,6 +352,9 @@ def main():
             "kernel_share_of_step": round(td["ms"] / sum(v["ms"] for v in timing.values() if v["launches"]), 4),
             "step_frac_of_roofline": round(value * B / 1e9 / peak, 4),
             "bytes_per_point_step": B}
+    if B_fused:
+        roof["fused_bytes_per_point_step"] = B_fused
+        roof["step_frac_of_fused_roofline"] = round(value * B_fused / 1e9 / peak, 4)
 
     # e2e: the paper's chunk model through the public API with host buffers: per chunk of
     # `steps` RK4 steps, H2D of Psi from pinned memory, the steps, D2H of Psi to pinned memory.

@@ -201,7 +201,7 @@ nlse_status nlse_get_stream(nlse_ctx *ctx, void **stream);
  * kind.  Adds one event pair per launch; off by default. */
 nlse_status nlse_set_timing(nlse_ctx *ctx, int enable);
 
-#define NLSE_MAX_KINDS 8
+#define NLSE_MAX_KINDS 12
 typedef struct {
     int n_kinds;
     char name[NLSE_MAX_KINDS][48];       /* kernel kind, e.g. "stage3d_stream" */

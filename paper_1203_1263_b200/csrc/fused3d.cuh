@@ -27,19 +27,28 @@
 
 namespace nlse {
 
-template <typename T, int TYV>
+#ifndef NLSE_FUSED_P
+#define NLSE_FUSED_P 2
+#endif
+#ifndef NLSE_FUSED_MINB
+#define NLSE_FUSED_MINB 1
+#endif
+template <typename T, int TYV, int PAIR = 2>
 struct F3Cfg {
-    static constexpr int TX = 32, TY = TYV, NT = TX * TY;
+    static constexpr int TX = 32, TY = TYV;
     static constexpr int RX = TX + 2, RY = TY + 2, RS = RX * RY;    // region R (stage A outputs)
+    static constexpr int NT = (RS + 31) / 32 * 32;                  // one thread per point of R
     static constexpr int YX = TX + 4, YY = TY + 4;                  // Y_A box, origin (x0-2, y0-2)
     static constexpr int BX = TX + 4, BY = RY;                      // base box (complex), origin (x0-2, y0-1)
     static constexpr int VXO = sizeof(T) == 4 ? 4 : 2;              // V box origin x0 - VXO (16-byte aligned)
     static constexpr int VX = TX + 2 * VXO, VY = RY;
     static constexpr int CB = 2 * int(sizeof(T));
-    static constexpr int P = 2;                                     // planes of prefetch
+    // ring sizes: a slot is refilled one plane after its last reader (single barrier per plane)
+    static constexpr int P = NLSE_FUSED_P;                          // planes of prefetch
     static constexpr int NSY = P + 3;                               // Y_A ring (planes p-1, p, p+1 + P)
     static constexpr int NSV = P + 2;                               // V / base ring (planes z, p + P)
     static constexpr int NSK = P + 1;                               // K ring (plane z + P)
+    static constexpr int NZ = 4;                                    // Z ring (planes z-1, z, z+1 + one being written)
     static constexpr int up128(int b) { return (b + 127) / 128 * 128; }
     static constexpr int YSLOT = up128(YX * YY * CB);
     static constexpr int VSLOT = up128(VX * VY * int(sizeof(T)));
@@ -48,10 +57,9 @@ struct F3Cfg {
     static constexpr int RSLOT = up128(RS * CB);
     static constexpr int OFF_V = NSY * YSLOT;
     static constexpr int OFF_B = OFF_V + NSV * VSLOT;
-    static constexpr int OFF_K = OFF_B + NSV * BSLOT;
-    static constexpr int OFF_F = OFF_K + NSK * KSLOT;               // 2 slots: F_A of planes by parity
-    static constexpr int OFF_Z = OFF_F + 2 * RSLOT;                 // 3 slots: Z of planes p mod 3
-    static constexpr int OFF_BAR = OFF_Z + 3 * RSLOT;
+    static constexpr int OFF_K = OFF_B + (PAIR == 2 ? NSV * BSLOT : 0);   // base and K: pair 2 only
+    static constexpr int OFF_Z = OFF_K + (PAIR == 2 ? NSK * KSLOT : 0);
+    static constexpr int OFF_BAR = OFF_Z + NZ * RSLOT;
     static constexpr int SMEM = OFF_BAR + (NSY + NSV + NSK) * 8;
     // box dimensions in T elements (x) and rows
     static constexpr int BOX_Y_X = 2 * YX, BOX_Y_Y = YY;
@@ -70,14 +78,14 @@ struct FusedArgs {
 // One fused pass.  PAIR 1: Y_A = base = Psi (mY), out = Psi_out, K written.  PAIR 2: Y_A = Psi_out
 // (mY), base = Psi (mB), K read (mK), out = the other Psi buffer.
 template <typename T, int BC, int PAIR, int TYV>
-__global__ void __launch_bounds__(32 * TYV, 1)
+__global__ void __launch_bounds__(F3Cfg<T, TYV>::NT, NLSE_FUSED_MINB)
 fused3d_cd(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mB,
            const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
            const __grid_constant__ StageArgs<T> A, const __grid_constant__ FusedArgs<T> FA, int zchunk, int ntx,
            int nty) {
     using C = cplx<T>;
-    using Cfg = F3Cfg<T, TYV>;
-    constexpr int TX = Cfg::TX, TY = Cfg::TY, NT = Cfg::NT, RX = Cfg::RX, RS = Cfg::RS;
+    using Cfg = F3Cfg<T, TYV, PAIR>;
+    constexpr int TX = Cfg::TX, TY = Cfg::TY, RX = Cfg::RX, RS = Cfg::RS;
     constexpr int YX = Cfg::YX, BX = Cfg::BX, VX = Cfg::VX, VXO = Cfg::VXO;
     constexpr int NSY = Cfg::NSY, NSV = Cfg::NSV, NSK = Cfg::NSK, P = Cfg::P;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -162,12 +170,15 @@ fused3d_cd(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUten
     auto Kp = [&](int z) -> const C * {                      // K at owned (lx, ly): [ly*TX + lx]
         return reinterpret_cast<const C *>(sm + Cfg::OFF_K + ((z - zs) % NSK) * Cfg::KSLOT);
     };
-    auto Fs = [&](int p) -> C * {                            // F_A on R: [(ly+1)*RX + lx+1]
-        return reinterpret_cast<C *>(sm + Cfg::OFF_F + (p & 1) * Cfg::RSLOT) + RX + 1;
+    // the same views by ring slot index (the loop advances the slot indices incrementally)
+    auto Ys = [&](int sl) -> const C * { return reinterpret_cast<const C *>(sm + sl * Cfg::YSLOT) + 2 * YX + 2; };
+    auto Vs = [&](int sl) -> const T * {
+        return reinterpret_cast<const T *>(sm + Cfg::OFF_V + sl * Cfg::VSLOT) + VX + VXO;
     };
-    auto Zs = [&](int p) -> C * {                            // Z on R
-        return reinterpret_cast<C *>(sm + Cfg::OFF_Z + (((p % 3) + 3) % 3) * Cfg::RSLOT) + RX + 1;
+    auto Bs = [&](int sl) -> const C * {
+        return reinterpret_cast<const C *>(sm + Cfg::OFF_B + sl * Cfg::BSLOT) + BX + 2;
     };
+    auto Zsl = [&](int sl) -> C * { return reinterpret_cast<C *>(sm + Cfg::OFF_Z + sl * Cfg::RSLOT) + RX + 1; };
     const T s_ = A.c.s, a_ = A.c.a, ih2 = A.c.ih2;
     // F (fsplit) P:424-428 at one point, R-ASSOC
     auto fsplit = [&](C y, C L, T v) -> C {
@@ -191,86 +202,74 @@ fused3d_cd(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUten
     auto vat = [&](int p, int lx, int ly) -> T { return hasV ? Vp(p)[ly * VX + lx] : T(0); };
     auto zface = [&](int p) { return (g.zf_lo && p == 0) || (g.zf_hi && p == nz - 1); };
 
-    // A, pass 1: F_A at the in-plane interior points of R on a non-face plane p
-    auto a_interior = [&](int p) {
-        const C *ym = Yp(p - 1), *yc = Yp(p), *yp = Yp(p + 1);
-        C *F = Fs(p);
-        for (int e = tid; e < RS; e += NT) {
-            const int lx = e % RX - 1, ly = e / RX - 1;
-            const int gx = x0 + lx, gy = y0 + ly;
-            if (gx < 1 || gx > nx - 2 || gy < 1 || gy > ny - 2) continue;
-            const int o = ly * YX + lx;
-            F[ly * RX + lx] = fsplit(yc[o], cd(ym, yc, yp, o, YX), vat(p, lx, ly));
-        }
+    // Thread t owns point t of the ring region R (local (lx, ly) = (t % RX - 1, t / RX - 1)) in
+    // stage A and, when that point is one of the tile's own interior points, in stage B too, so
+    // F_A of its point stays in a register from A(z) to B(z).
+    const int lx = tid % RX - 1, ly = tid / RX - 1;
+    const int gx = x0 + lx, gy = y0 + ly;
+    const bool in_r = tid < RS && gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+    const bool fx = gx == 0 || gx == nx - 1, fy = gy == 0 || gy == ny - 1;
+    const bool interior = in_r && !fx && !fy;
+    const bool owned = in_r && lx >= 0 && lx < TX && ly >= 0 && ly < TY;
+    const bool outpt = owned && interior;                          // a stage-B output point
+    const int lx1 = gx == 0 ? lx + 1 : (gx == nx - 1 ? lx - 1 : lx);  // b': one step inward
+    const int ly1 = gy == 0 ? ly + 1 : (gy == ny - 1 ? ly - 1 : ly);  //     along every face axis
+    const int oy = ly * YX + lx, oy1 = ly1 * YX + lx1, orr = ly * RX + lx;
+    const int64_t qrow = int64_t(gy) * g.sy + gx;
+    const bool shell_xy = gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2;
+    // F_A at an in-plane interior point (CD, (fsplit)) of plane p, Y-box offset o, V offset (x, y)
+    auto f_int = [&](int p, int o, int vx, int vy) -> C {
+        return fsplit(Yp(p)[o], cd(Yp(p - 1), Yp(p), Yp(p + 1), o, YX), vat(p, vx, vy));
     };
-    // A, pass 2: face F_A (the BC form, b' one step inward along every boundary axis, R-MSD-NBR),
-    // Z = base + c_A F_A on R, and the boundary data the stage-B boundary kernel reads
-    auto a_finish = [&](int p) {
+    // Stage A at this thread's point of plane p: F_A (faces by the BC time-derivative form with
+    // F_A(b') recomputed here, b' on plane pb), Z = base + c_A F_A into the Z slot of plane p,
+    // and the boundary data of the stage-B boundary kernel at this CTA's own points.
+    // ym, yc, yp: Y_A slots of planes p-1, p, p+1; vc: V slot of p (or null); bc_: base slot of p;
+    // zo: Z slot of plane p
+    auto stage_a = [&](int p, const C *ym, const C *yc, const C *yp, const T *vc, const C *bc_, C *zo) -> C {
+        C f; f.x = T(0); f.y = T(0);
+        if (!in_r) return f;
         const bool zf = zface(p);
-        const int pb = zf ? (p == 0 ? 1 : nz - 2) : p;           // plane of b'
-        const C *yc = Yp(p), *y1p = Yp(pb);
-        C *F = Fs(p);
-        const C *F1 = Fs(pb);
-        C *Z = Zs(p);
-        const bool own_plane = (p >= zs && p < ze) || zf;
-        for (int e = tid; e < RS; e += NT) {
-            const int lx = e % RX - 1, ly = e / RX - 1;
-            const int gx = x0 + lx, gy = y0 + ly;
-            if (gx < 0 || gx >= nx || gy < 0 || gy >= ny) continue;
-            const bool fx = gx == 0 || gx == nx - 1, fy = gy == 0 || gy == ny - 1;
-            const int r = ly * RX + lx;
-            const C y = yc[ly * YX + lx];
-            C f;
-            const bool face = zf || fx || fy;
-            if (!face) {
-                f = F[r];
-            } else if (BC == BC_DIRICHLET) {
-                f.x = T(0); f.y = T(0);                               // (BCDdt) P:315-318
-            } else if (BC == BC_L0) {
-                C zr; zr.x = T(0); zr.y = T(0);
-                f = fsplit(y, zr, vat(p, lx, ly));                    // (BCL0dt) P:347-350, R-L0
-            } else {                                                  // (msd) P:331-335
-                const int lx1 = gx == 0 ? lx + 1 : (gx == nx - 1 ? lx - 1 : lx);
-                const int ly1 = gy == 0 ? ly + 1 : (gy == ny - 1 ? ly - 1 : ly);
-                const C y1 = y1p[ly1 * YX + lx1], f1 = F1[ly1 * RX + lx1];
-                const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
-                T m = T(0);
-                if (!(rho1 < A.c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
-                f.x = -(m * y.y);
-                f.y = m * y.x;
-            }
-            const C base = PAIR == 1 ? y : Bp(p)[ly * BX + lx];
-            const C z = cfma(FA.cA, f, base);
-            Z[r] = z;
-            if (face && !zf) F[r] = f;                                // F_A of x/y faces (K of face points)
-            // boundary data for the stage-B boundary kernel, at this CTA's own points
-            const bool owned = lx >= 0 && lx < TX && ly >= 0 && ly < TY && own_plane;
-            if (!owned) continue;
-            const int64_t q = int64_t(p) * g.sz + int64_t(gy) * g.sy + gx;
-            const bool shell = !face && (gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2 ||
-                                         (g.zf_lo && p == 1) || (g.zf_hi && p == nz - 2));
+        const C y = yc[oy];
+        const bool face = zf || fx || fy;
+        if (!face) {
+            f = fsplit(y, cd(ym, yc, yp, oy, YX), hasV ? vc[ly * VX + lx] : T(0));
+        } else if (BC == BC_L0) {
+            C zr; zr.x = T(0); zr.y = T(0);
+            f = fsplit(y, zr, vat(p, lx, ly));                        // (BCL0dt) P:347-350, R-L0
+        } else if (BC == BC_MSD) {                                    // (msd) P:331-335
+            const int pb = zf ? (p == 0 ? 1 : nz - 2) : p;
+            const C y1 = Yp(pb)[oy1];
+            const C f1 = f_int(pb, oy1, lx1, ly1);
+            const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+            T m = T(0);
+            if (!(rho1 < A.c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
+            f.x = -(m * y.y);
+            f.y = m * y.x;
+        }                                                             // Dirichlet: 0 (BCDdt) P:315-318
+        const C base = PAIR == 1 ? y : bc_[ly * BX + lx];
+        const C z = cfma(FA.cA, f, base);
+        zo[orr] = z;
+        if (owned && ((p >= zs && p < ze) || zf)) {
+            const int64_t q = int64_t(p) * g.sz + qrow;
+            const bool shell = !face && (shell_xy || (g.zf_lo && p == 1) || (g.zf_hi && p == nz - 2));
             if (face || shell) FA.ztmp[q] = z;
             if (face) A.K[q] = PAIR == 1 ? f : cfma(T(2), f, __ldg(A.K + q));
         }
+        return f;
     };
-    // B: F_B on the owned interior points of plane z, the stage-B combine, MSD F_B at b'
-    auto b_stage = [&](int z) {
-        const C *zm = Zs(z - 1), *zc = Zs(z), *zp = Zs(z + 1);
-        const C *F = Fs(z);
-        const int lx = tid & 31, ly = tid >> 5;
-        const int gx = x0 + lx, gy = y0 + ly;
-        if (gx < 1 || gx > nx - 2 || gy < 1 || gy > ny - 2) return;
-        const int r = ly * RX + lx;
-        const C y = zc[r];
-        const C fb = fsplit(y, cd(zm, zc, zp, r, RX), vat(z, lx, ly));
-        const C fa = F[r];
-        const int64_t q = int64_t(z) * g.sz + int64_t(gy) * g.sy + gx;
+    // Stage B at this thread's own interior point of plane z (F_A of that point given)
+    // zm, zc, zp: Z slots of planes z-1, z, z+1; yz: Y_A slot of z; vz, bz: V / base slots of z
+    auto stage_b = [&](int z, C fa, const C *zm, const C *zc, const C *zp, const C *yz, const T *vz, const C *bz) {
+        const C y = zc[orr];
+        const C fb = fsplit(y, cd(zm, zc, zp, orr, RX), hasV ? vz[ly * VX + lx] : T(0));
+        const int64_t q = int64_t(z) * g.sz + qrow;
         if (PAIR == 1) {
-            const C psi = Yp(z)[ly * YX + lx];
+            const C psi = yz[oy];
             A.K[q] = cfma(T(2), fb, fa);                              // S2: K = 2 F_B + F_A (S1: K = F_A)
             A.out[q] = cfma(A.c.kc, fb, psi);                         // Psi_out = Psi + (k/2) F_B
         } else {
-            const C psi = Bp(z)[ly * BX + lx];
+            const C psi = bz[ly * BX + lx];
             const C kt = cfma(T(2), fa, Kp(z)[ly * TX + lx]);        // S3: K = 2 F_A + K
             const C o = cfma(A.c.kc, cadd(kt, fb), psi);              // S4: Psi + (k/6)(K + F_B)
             A.out[q] = o;
@@ -279,37 +278,46 @@ fused3d_cd(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUten
         if (A.fp) {                                                   // F_B at b' for the MSD light pass
             if (g.zf_lo && z == 1) A.fz[gy * nx + gx] = fb;
             if (g.zf_hi && z == nz - 2) A.fz[int64_t(nx) * ny + gy * nx + gx] = fb;
-            if (gx == 1 || gx == nx - 2 || gy == 1 || gy == ny - 2) A.fp[int64_t(z) * A.per2 + shell_u(gx, gy, nx, ny)] = fb;
+            if (shell_xy) A.fp[int64_t(z) * A.per2 + shell_u(gx, gy, nx, ny)] = fb;
         }
     };
 
     // ---- prologue: stage A on planes zs-1 (a z face when zs == 1) and zs ----
     wait_y(zs - 2); wait_y(zs - 1); wait_y(zs); wait_y(zs + 1);
     wait_v(zs - 1); wait_v(zs);
-    if (!zface(zs - 1)) a_interior(zs - 1);
-    a_interior(zs);
+    // Z ring: planes z-1, z, z+1 in slots zm1, z0s, zp1; zfr is written next (plane z+2)
+    int zm1 = 0, z0s = 1, zp1 = 2, zfr = 3;
+    stage_a(zs - 1, Yp(zs - 2), Yp(zs - 1), Yp(zs), hasV ? Vp(zs - 1) : nullptr, Bp(zs - 1), Zsl(zm1));
+    C fa = stage_a(zs, Yp(zs - 1), Yp(zs), Yp(zs + 1), hasV ? Vp(zs) : nullptr, Bp(zs), Zsl(z0s));
     __syncthreads();
-    a_finish(zs);                       // x/y faces of plane zs use F_A(zs) only
-    __syncthreads();
-    a_finish(zs - 1);                   // a z face takes F_A(zs) at b'; otherwise F_A(zs-1)
-    __syncthreads();
+    if (tid == 0) {                     // the prologue-only planes zs-2 (Y_A) and zs-1 (V / base) are free
+        issue_y(zs - 2 + NSY);
+        issue_v(zs - 1 + NSV);
+    }
+    // ring slots of plane z (Y_A, V / base) and of Z planes z-1, z, z+1, advanced per plane
+    int sy0 = (zs - ylo) % NSY, sv0 = (zs - vlo) % NSV;
+    auto nxt = [](int sl, int n) { return sl + 1 == n ? 0 : sl + 1; };
     for (int z = zs; z < ze; z++) {
         const int p = z + 1;
-        const bool zf = zface(p);
-        if (!zf) wait_y(p + 1);
+        if (!zface(p)) wait_y(p + 1);
         wait_v(p);
         wait_k(z);
-        if (!zf) a_interior(p);
+        const int sy1 = nxt(sy0, NSY), sy2 = nxt(sy1, NSY), sv1 = nxt(sv0, NSV);
+        // top z face: b' on plane p - 1 = z (its Y / V slots are intact)
+        const C fa_next = stage_a(p, Ys(sy0), Ys(sy1), Ys(sy2), hasV ? Vs(sv1) : nullptr, Bs(sv1), Zsl(zp1));
+        // the one barrier per plane: Z(z+1) is complete, and every thread has finished iteration
+        // z-1, so the slots whose last reader was B(z-1) / A(z) are free: Y_A(z-1), V / base(z-1),
+        // K(z-1) (the Z slot written next iteration held plane z-2, read last by B(z-1))
         __syncthreads();
-        a_finish(p);                    // top z face: b' on plane p - 1 = z (its F_A slot is intact)
-        __syncthreads();
-        b_stage(z);
-        __syncthreads();                // every read of the slots of plane z - 1 / z is done
         if (tid == 0) {
-            issue_y(z - 1 + NSY);       // Y_A(z-1) is free (next: A(z+2) needs z+1 .. z+3, B(z+1) z+1)
-            issue_v(z + NSV);           // V / base of plane z are free
-            issue_k(z + NSK);
+            issue_y(z - 1 + NSY);
+            if (z > zs) issue_v(z - 1 + NSV);   // (V / base(zs-1) was refilled after the prologue;
+            if (z > zs) issue_k(z - 1 + NSK);   //  K has no plane zs-1)
         }
+        if (outpt) stage_b(z, fa, Zsl(zm1), Zsl(z0s), Zsl(zp1), Ys(sy0), hasV ? Vs(sv0) : nullptr, Bs(sv0));
+        fa = fa_next;
+        sy0 = sy1; sv0 = sv1;
+        { const int t = zm1; zm1 = z0s; z0s = zp1; zp1 = zfr; zfr = t; }
     }
 }
 

@@ -3,3 +3,6 @@
 #include "stages.cuh"
 
 NLSE_DEFINE_STAGES(f32, 3, cd)
+NLSE_DEFINE_FUSED(f32, dirichlet)
+NLSE_DEFINE_FUSED(f32, msd)
+NLSE_DEFINE_FUSED(f32, l0)

@@ -3,3 +3,6 @@
 #include "stages.cuh"
 
 NLSE_DEFINE_STAGES(f64, 3, cd)
+NLSE_DEFINE_FUSED(f64, dirichlet)
+NLSE_DEFINE_FUSED(f64, msd)
+NLSE_DEFINE_FUSED(f64, l0)

@@ -11,6 +11,7 @@
 #include "generic.cuh"
 #include "persist1d.cuh"
 #include "stage3d_tma.cuh"
+#include "fused3d.cuh"
 
 using namespace nlse;
 using namespace nlse_rt;
@@ -22,7 +23,7 @@ thread_local std::string nlse_rt::g_create_error;
 namespace {
 
 const char *kKindName[KK_COUNT] = {"stage_generic", "stage3d_stream", "stage3d_tma", "stage2d_tile",
-                                   "stage1d_tile", "stage_boundary", "diag", "peer_barrier"};
+                                   "stage1d_tile", "stage_boundary", "diag", "peer_barrier", "fused3d_cd"};
 
 struct DistBlob {               // what nlse_dist_export writes (NLSE_DIST_HANDLE_BYTES)
     uint32_t magic, version;
@@ -84,6 +85,24 @@ bool make_map(CUtensorMap *m, void *base, int eb, uint64_t d0, uint64_t d1, uint
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// Fused mode (fused3d.cuh): Y_A box maps over all four halo'd buffers, the ring-R base box over
+// the Psi buffers, K over the owned box, V over the ring-R box (16-byte-aligned x origin).
+template <typename T, int TYV>
+bool build_fused_maps(nlse_ctx *c) {
+    using Cfg = F3Cfg<T, TYV>;
+    const uint64_t nx = c->g.nx, ny = c->g.ny, nz = c->g.nz, sy = c->g.sy;
+    const int eb = int(sizeof(T));
+    bool ok = true;
+    for (int b = 0; b < 4; b++) {
+        ok = ok && make_map(&c->fmaps.y[b], c->alloc[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
+        ok = ok && make_map(&c->fmaps.base[b], c->alloc[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_B_X, Cfg::BOX_B_Y);
+    }
+    ok = ok && make_map(&c->fmaps.k, c->K, eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_K_X, Cfg::BOX_K_Y);
+    if (c->V) ok = ok && make_map(&c->fmaps.v, c->V, eb, nx, ny, nz, sy, Cfg::BOX_V_X, Cfg::BOX_V_Y);
+    else c->fmaps.v = c->fmaps.k;   // never dereferenced without a V array
+    return ok;
 }
 
 template <typename T, int ORDER, int TYV>
@@ -192,11 +211,27 @@ nlse_status check_step_args(nlse_ctx *c, double k, int64_t nsteps) {
     return NLSE_OK;
 }
 
+FusedStepFn fused_fn(const nlse_ctx *c) {
+    const bool f64 = c->prec == NLSE_FP64;
+    if (c->bc == NLSE_BC_MSD) return f64 ? &fused_step_f64_msd : &fused_step_f32_msd;
+    if (c->bc == NLSE_BC_L0) return f64 ? &fused_step_f64_l0 : &fused_step_f32_l0;
+    return f64 ? &fused_step_f64_dirichlet : &fused_step_f32_dirichlet;
+}
+
 // Enqueue one RK4 stage of step n of the current launch sequence, followed (slab mode)
 // by the neighbour barrier (mode as enqueue_barrier).
 void enqueue_step_stage(nlse_ctx *c, int stage, double k, int64_t n, int mode = 3) {
     enqueue_stage(c, stage, k, int(std::min<int64_t>(n, INT32_MAX / 2)));
     enqueue_barrier(c, false, mode);
+}
+
+// One RK4 step: four stage launches, or (fused mode) two fused two-stage passes.
+void enqueue_one_step(nlse_ctx *c, double k, int64_t n) {
+    if (c->fused) {
+        fused_fn(c)(c, k, int(std::min<int64_t>(n, INT32_MAX / 2)));
+        return;
+    }
+    for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
 }
 
 void enqueue_add_steps(nlse_ctx *c, int64_t n) {
@@ -220,15 +255,15 @@ void drop_graph(nlse_ctx *c) {
 // Capture GRAPH_STEPS steps (all launches, barriers and the step-counter update) once
 // per k; false if capture is unavailable (then the caller launches directly).
 bool ensure_graph(nlse_ctx *c, double k) {
-    if (c->graph_exec && c->graph_k == k) return true;
+    if (c->graph_exec && c->graph_k == k && c->graph_parity == c->swap_parity) return true;
     drop_graph(c);
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    for (int n = 0; n < GRAPH_STEPS; n++)
-        for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+    const int parity0 = c->swap_parity;
+    for (int n = 0; n < GRAPH_STEPS; n++) enqueue_one_step(c, k, n);
     enqueue_add_steps(c, GRAPH_STEPS);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph_exec, g, 0);
@@ -239,6 +274,7 @@ bool ensure_graph(nlse_ctx *c, double k) {
         return false;
     }
     c->graph_k = k;
+    c->graph_parity = parity0;     // GRAPH_STEPS is even: replaying it leaves the Psi buffers in place
     return true;
 }
 
@@ -567,6 +603,26 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
             CREATE_TRY(cudaMalloc(&c->fp, fpb));
             c->device_bytes += int64_t(fzb + fpb);
         }
+        // temporal blocking (§8(f) rank 2, fused3d.cuh): S1+S2 and S3+S4 in one HBM pass each; 3D
+        // CD on one GPU; MSD needs the stored-F(b') boundary pass.  Default: fp64 grids of >= 2^26
+        // points, where it measured faster (r02f: 1024^3 46.3 vs 54.6 ms/step); the L2-scale and
+        // fp32 grids stay on the single-stage kernel.  NLSE_FUSED=1 / 0 forces it on / off.
+        const char *efu = getenv("NLSE_FUSED");
+        const bool want_fused = efu ? efu[0] == '1' : (prec == NLSE_FP64 && n >= (int64_t(1) << 26));
+        if (ok && want_fused && order == NLSE_CD2 && !dist && (bc != NLSE_BC_MSD || c->fp)) {
+            CREATE_TRY(cudaMalloc(&c->alloc[BUF_PSI2], halo_bytes));
+            CREATE_TRY(cudaMemsetAsync(c->alloc[BUF_PSI2], 0, halo_bytes, c->stream));
+            c->buf[BUF_PSI2] = c->alloc[BUF_PSI2];
+            c->device_bytes += int64_t(halo_bytes);
+            const char *fty = getenv("NLSE_FUSED_TY");
+            c->fused_ty = (fty && std::atoi(fty) == 8) ? 8 : 16;
+            bool fok;
+            if (prec == NLSE_FP64)
+                fok = c->fused_ty == 16 ? build_fused_maps<double, 16>(c) : build_fused_maps<double, 8>(c);
+            else
+                fok = c->fused_ty == 16 ? build_fused_maps<float, 16>(c) : build_fused_maps<float, 8>(c);
+            c->fused = fok;
+        }
     }
 #undef CREATE_TRY
     c->persist1d = use_persist1d(c);
@@ -591,8 +647,7 @@ nlse_status enqueue_steps(nlse_ctx *c, double k, int64_t nsteps) {
             CUDA_TRY(c, cudaGraphLaunch(c->graph_exec, c->stream));
     }
     if (done < nsteps) {
-        for (int64_t n = 0; n < nsteps - done; n++)
-            for (int s = 1; s <= 4; s++) enqueue_step_stage(c, s, k, n);
+        for (int64_t n = 0; n < nsteps - done; n++) enqueue_one_step(c, k, n);
         enqueue_add_steps(c, nsteps - done);
     }
     return NLSE_OK;
@@ -645,7 +700,7 @@ void nlse_destroy(nlse_ctx *c) {
     for (auto &t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
     for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
-    for (int b = 0; b < 3; b++) cudaFree(c->alloc[b]);
+    for (int b = 0; b < 4; b++) cudaFree(c->alloc[b]);
     cudaFree(c->K); cudaFree(c->V); cudaFree(c->comm); cudaFree(c->fz); cudaFree(c->fp);
     drop_graph(c);
     cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result);
@@ -983,12 +1038,13 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     out->points = c->g.n;
     int per_stage = c->interior_kind == KK_GENERIC ? 1 : 2;
     if (c->dist && c->nranks > 1) per_stage += 1;
-    out->launches_per_step = c->persist1d ? 0 : 4 * per_stage;   // 0: one launch per nlse_step call
+    out->launches_per_step = c->persist1d ? 0 : (c->fused ? 4 : 4 * per_stage);   // 0: one launch per nlse_step call
     const int64_t cbytes = 2 * c->eb, rv = c->hasV ? c->eb : 0;
     out->min_bytes_per_step = (16 * cbytes + 4 * rv) * c->g.n;
     out->device_bytes = c->device_bytes;
     out->elem_bytes = c->eb;
-    snprintf(out->variant, sizeof out->variant, "%s", c->persist1d ? "rk4_1d_persistent" : kKindName[c->interior_kind]);
+    snprintf(out->variant, sizeof out->variant, "%s",
+             c->persist1d ? "rk4_1d_persistent" : (c->fused ? kKindName[KK_FUSED3D] : kKindName[c->interior_kind]));
     out->rank = c->rank;
     out->nranks = c->nranks;
     out->z0 = c->z0;

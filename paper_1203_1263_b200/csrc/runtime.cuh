@@ -10,6 +10,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda.h>
@@ -19,7 +20,8 @@
 #include "comm.cuh"
 #include "common.cuh"
 
-enum KernelKind { KK_GENERIC = 0, KK_STREAM3D, KK_TMA3D, KK_TILE2D, KK_TILE1D, KK_BOUNDARY, KK_DIAG, KK_COMM, KK_COUNT };
+enum KernelKind { KK_GENERIC = 0, KK_STREAM3D, KK_TMA3D, KK_TILE2D, KK_TILE1D, KK_BOUNDARY, KK_DIAG, KK_COMM,
+                  KK_FUSED3D, KK_COUNT };
 static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
 
 struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };
@@ -32,12 +34,21 @@ struct Tma3Maps {
     CUtensorMap psi, k, v;
 };
 
+// TMA descriptors of the fused two-stage kernel (fused3d.cuh): the Y_A box over every halo'd
+// buffer (index = buffer, 3 = the second Psi buffer), the ring-R base box over the two Psi
+// buffers, K over the owned box, V over the ring-R box.
+struct FusedMaps {
+    CUtensorMap y[4];
+    CUtensorMap base[4];
+    CUtensorMap k, v;
+};
+
 struct StreamHolder {
     cudaStream_t s = nullptr;
     ~StreamHolder() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
 };
 
-enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2 };
+enum { BUF_PSI = 0, BUF_TMP = 1, BUF_OUT = 2, BUF_PSI2 = 3 };   // BUF_PSI2: fused mode's Psi ping-pong
 
 struct nlse_ctx {
     int ndim = 0;
@@ -52,8 +63,8 @@ struct nlse_ctx {
     bool hasV = false;
     bool pitched = false;            // rows padded to g.sy > nx points (16-byte TMA strides)
     // halo'd buffers: allocation base (plane -zghost) and plane-0 pointer
-    void *alloc[3] = {nullptr, nullptr, nullptr};
-    void *buf[3] = {nullptr, nullptr, nullptr};
+    void *alloc[4] = {nullptr, nullptr, nullptr, nullptr};
+    void *buf[4] = {nullptr, nullptr, nullptr, nullptr};
     void *K = nullptr, *V = nullptr;
     void *fz = nullptr, *fp = nullptr;   // MSD 3D TMA path: stored F(b') (see StageArgs)
     int per2 = 0;
@@ -91,6 +102,12 @@ struct nlse_ctx {
     bool tma = false;
     int tma_ty = 8;                  // TMA kernel tile height (8: 256 threads, 16: 512 threads)
     Tma3Maps maps{};
+    // temporal blocking (§8(f) rank 2, fused3d.cuh): two RK4 stages per HBM pass, 3D CD, one GPU
+    bool fused = false;
+    int fused_ty = 16;
+    FusedMaps fmaps{};
+    int swap_parity = 0;             // Psi buffers swapped an odd number of times (fused mode)
+    int graph_parity = 0;            // swap_parity when the CUDA graph was captured
     // slab mode
     bool dist = false;
     int rank = 0, nranks = 1;
@@ -199,6 +216,22 @@ using EnqueueStageFn = void (*)(nlse_ctx *, int stage, double k, int step);
 // 1D: all nsteps in one persistent CTA (persist1d.cuh)
 using Persist1DFn = void (*)(nlse_ctx *, double k, int64_t nsteps);
 using Persist1DSmemFn = size_t (*)(const nlse_ctx *);
+// fused mode: one RK4 step (two fused passes + their boundary passes), then the Psi swap
+using FusedStepFn = void (*)(nlse_ctx *, double k, int step);
+void fused_step_f64_dirichlet(nlse_ctx *, double, int);
+void fused_step_f64_msd(nlse_ctx *, double, int);
+void fused_step_f64_l0(nlse_ctx *, double, int);
+void fused_step_f32_dirichlet(nlse_ctx *, double, int);
+void fused_step_f32_msd(nlse_ctx *, double, int);
+void fused_step_f32_l0(nlse_ctx *, double, int);
+// Swap the two Psi buffers (fused mode, after each step's second pass).
+inline void swap_psi(nlse_ctx *c) {
+    std::swap(c->alloc[BUF_PSI], c->alloc[BUF_PSI2]);
+    std::swap(c->buf[BUF_PSI], c->buf[BUF_PSI2]);
+    std::swap(c->fmaps.y[BUF_PSI], c->fmaps.y[BUF_PSI2]);
+    std::swap(c->fmaps.base[BUF_PSI], c->fmaps.base[BUF_PSI2]);
+    c->swap_parity ^= 1;
+}
 
 #define NLSE_FAMILIES(X)                                                                        \
     X(f64, 1, cd) X(f64, 1, shoc) X(f64, 2, cd) X(f64, 2, shoc) X(f64, 3, cd) X(f64, 3, shoc)  \

@@ -10,6 +10,7 @@
 #include "stage3d_tma.cuh"
 #include "stream3d.cuh"
 #include "tile2d.cuh"
+#include "fused3d.cuh"
 
 namespace nlse_rt {
 
@@ -209,6 +210,83 @@ void launch_persist1d(nlse_ctx *c, double k, int64_t nsteps) {
     rk4_1d_persistent<T, ORDER, BC><<<1, P1_THREADS, smem, c->stream>>>(P);
 }
 
+// ------------------------------------------------------------------ fused two-stage passes
+// One RK4 step in fused mode (§8(f) rank 2, fused3d.cuh): pass 1 = S1+S2, pass 2 = S3+S4, each
+// followed by the boundary kernel of its second stage; Psi_new goes to the second Psi buffer and
+// the two Psi buffers are swapped.
+template <typename T, int BC, int PAIR, int TYV>
+void launch_fused_pass(nlse_ctx *c, double k, int step) {
+    using C = cplx<T>;
+    using Cfg = F3Cfg<T, TYV, PAIR>;
+    constexpr int STAGE_B = PAIR == 1 ? 2 : 4;
+    auto kern = fused3d_cd<T, BC, PAIR, TYV>;
+    StageArgs<T> A{};
+    A.Y = (const C *)c->buf[BUF_TMP];                 // stage-B input at face / b' points (boundary pass)
+    A.Psi = (const C *)c->buf[BUF_PSI];
+    A.K = (C *)c->K;
+    A.out = (C *)c->buf[PAIR == 1 ? BUF_OUT : BUF_PSI2];
+    A.V = (const T *)c->V;
+    A.g = c->g;
+    A.c = make_consts<T>(c, PAIR == 1 ? k / 2.0 : k / 6.0);
+    A.diverged = c->d_div;
+    A.step_base = c->d_steps;
+    A.step = step;
+    A.wsend = 1;
+    A.fz = (C *)c->fz;
+    A.fp = (C *)c->fp;
+    A.per2 = c->per2;
+    A.xfuse = 0;
+    FusedArgs<T> FA{};
+    FA.cA = T(PAIR == 1 ? k / 2.0 : k);
+    FA.ztmp = (C *)c->buf[BUF_TMP];
+    const int64_t nx = c->g.nx, ny = c->g.ny, mz = c->g.nz - 2;
+    const unsigned gx = unsigned((nx + Cfg::TX - 1) / Cfg::TX), gy = unsigned((ny + Cfg::TY - 1) / Cfg::TY);
+    static PerDevice attr;
+    if (!attr.get(c->device)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        attr.set(c->device, 1);
+    }
+    // z chunks as launch_tma3d_ty: <= 128 planes, whole waves of one CTA per SM
+    const int64_t cols = int64_t(gx) * gy;
+    int64_t zchunk = mz, best = -1;
+    for (int64_t nzc = (mz + 127) / 128; nzc <= mz; nzc++) {
+        const int64_t ch = (mz + nzc - 1) / nzc;
+        const int64_t waves = (cols * nzc + c->nsm - 1) / c->nsm;
+        const int64_t cost = waves * (ch + 4);
+        if (best < 0 || cost < best) { best = cost; zchunk = ch; }
+        if (ch <= 4) break;
+    }
+    const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
+    const CUtensorMap &mY = c->fmaps.y[PAIR == 1 ? BUF_PSI : BUF_OUT];
+    {
+        LaunchTimer lt(c, KK_FUSED3D, (nx - 2) * (ny - 2) * mz);
+        kern<<<unsigned(cols * gz), Cfg::NT, Cfg::SMEM, c->stream>>>(mY, c->fmaps.base[BUF_PSI], c->fmaps.k,
+                                                                     c->fmaps.v, A, FA, int(zchunk), int(gx), int(gy));
+    }
+    // stage-B outputs at the domain boundary
+    if (BC == BC_MSD) {
+        const int64_t nb = n_boundary_points<3>(c->g, false);
+        LaunchTimer lt(c, KK_BOUNDARY, nb);
+        stage_boundary_msd_fb<T, STAGE_B><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
+    } else {
+        const int64_t nb = n_boundary_points<3>(c->g);
+        LaunchTimer lt(c, KK_BOUNDARY, nb);
+        stage_boundary<T, 3, ORDER_CD, BC, STAGE_B><<<blocks_for(nb, 256), 256, 0, c->stream>>>(A);
+    }
+}
+
+template <typename T, int BC>
+void fused_step_t(nlse_ctx *c, double k, int step) {
+    if (c->fused_ty == 8) {
+        launch_fused_pass<T, BC, 1, 8>(c, k, step);
+        launch_fused_pass<T, BC, 2, 8>(c, k, step);
+    } else {
+        launch_fused_pass<T, BC, 1, 16>(c, k, step);
+        launch_fused_pass<T, BC, 2, 16>(c, k, step);
+    }
+    swap_psi(c);
+}
+
 template <typename T, int ORDER>
 void persist1d_family(nlse_ctx *c, double k, int64_t nsteps) {
     if (c->bc == NLSE_BC_MSD) launch_persist1d<T, ORDER, BC_MSD>(c, k, nsteps);
@@ -235,4 +313,8 @@ void persist1d_family(nlse_ctx *c, double k, int64_t nsteps) {
 #define NLSE_DEFINE_PERSIST1D(P, O)                                                             \
     void nlse_rt::persist1d_##P##_##O(nlse_ctx *c, double k, int64_t nsteps) {                  \
         nlse_rt::persist1d_family<NLSE_REAL_##P, NLSE_ORDER_##O>(c, k, nsteps);                 \
+    }
+#define NLSE_DEFINE_FUSED(P, B)                                                                 \
+    void nlse_rt::fused_step_##P##_##B(nlse_ctx *c, double k, int step) {                       \
+        nlse_rt::fused_step_t<NLSE_REAL_##P, NLSE_BC_##B>(c, k, step);                           \
     }

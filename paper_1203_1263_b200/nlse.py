@@ -21,7 +21,7 @@ NLSE_BC_DIRICHLET, NLSE_BC_MSD, NLSE_BC_L0 = 0, 1, 2
 NLSE_CD2, NLSE_2SHOC4 = 2, 4
 NLSE_FP32, NLSE_FP64 = 4, 8
 NLSE_FLAG_FORCE_DT, NLSE_FLAG_GENERIC_KERNELS = 1, 2
-NLSE_MAX_KINDS = 8
+NLSE_MAX_KINDS = 12
 
 BC = {"dirichlet": NLSE_BC_DIRICHLET, "msd": NLSE_BC_MSD, "l0": NLSE_BC_L0}
 ORDER = {"cd": NLSE_CD2, "2shoc": NLSE_2SHOC4}
