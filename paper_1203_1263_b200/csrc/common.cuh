@@ -52,13 +52,25 @@ template <typename T> struct Consts {
 // The grid a context owns.  Single GPU: the whole grid.  Slab mode (§8(e)): the z
 // planes [z0, z0 + nz) of the global grid; the buffers read with a halo carry zghost
 // planes below plane 0 and above plane nz - 1, filled by the neighbours.
+// Slab mode partitions the slowest axis (the "slab axis": z in 3D, y in 2D): ns = its owned
+// length (nz in 3D, ny in 2D), su = the stride of one slab-axis step (sz in 3D, sy in 2D);
+// zf_lo / zf_hi / zghost refer to that axis.
 struct Grid {
-    int64_t nx, ny, nz;   // points per axis (unused = 1); nz = owned planes
-    int64_t sy, sz;       // strides: sy = nx, sz = nx*ny
+    int64_t nx, ny, nz;   // points per axis (unused = 1); 3D: nz = owned planes, 2D: ny = owned rows
+    int64_t sy, sz;       // strides: sy = nx (or the pitched row), sz = sy*ny
     int64_t n;            // owned points
-    int zf_lo, zf_hi;     // 1 if local plane 0 / nz - 1 is a global z face (always 1 on one GPU)
-    int zghost;           // ghost planes on each side of the halo'd buffers (0 on one GPU)
+    int zf_lo, zf_hi;     // 1 if local slab-axis index 0 / ns - 1 is a global face (always 1 on one GPU)
+    int zghost;           // ghost planes (3D) / rows (2D) on each side of the halo'd buffers (0 on one GPU)
+    int64_t ns, su;       // slab axis: owned length and stride (3D: nz, sz; 2D: ny, sy; 1D: 1, n)
 };
+
+// 2D y-slab face tests (3D grids keep y = 0 / ny - 1 as faces): the low / high row of the owned
+// rows is a domain face only where the slab holds the global face (zf_lo / zf_hi)
+template <int DIM>
+__host__ __device__ __forceinline__ bool y_face(const Grid &g, int64_t j) {
+    if (DIM == 2) return (g.zf_lo && j == 0) || (g.zf_hi && j == g.ny - 1);
+    return j == 0 || j == g.ny - 1;
+}
 
 // global z-face test for a local plane index (DIM == 3)
 __host__ __device__ __forceinline__ bool is_zface(const Grid &g, int64_t k) {
@@ -107,12 +119,13 @@ __host__ __device__ __forceinline__ int shell_u(int i, int j, int nx, int ny) {
     return 2 * (nx - 2) + 2 * (j - 2) + (i == nx - 2 ? 1 : 0);
 }
 
-// Store one stage output value at local point q of plane k (and into the neighbours' ghosts).
+// Store one stage output value at local point q, slab-axis index k (plane in 3D, row in 2D),
+// and into the neighbours' ghosts.
 template <typename T>
 __device__ __forceinline__ void store_out(const StageArgs<T> &A, int64_t q, int64_t k, cplx<T> v) {
     A.out[q] = v;
     if (A.peer_lo && k < A.wsend) A.peer_lo[q] = v;
-    if (A.peer_hi && k >= A.g.nz - A.wsend) A.peer_hi[q] = v;
+    if (A.peer_hi && k >= A.g.ns - A.wsend) A.peer_hi[q] = v;
 }
 
 // RK4 stage combine at one point, (RK4_GPU) P:495-519 / (RK4) P:164-180 (fused
@@ -121,7 +134,7 @@ __device__ __forceinline__ void store_out(const StageArgs<T> &A, int64_t q, int6
 //   S2: K = fma(2, F, K); out = fma(k/2, F, Psi)
 //   S3: K = fma(2, F, K); out = fma(k, F, Psi)
 //   S4:                   out = fma(k/6, K + F, Psi)
-// kz = local plane of q (for the neighbour stores; 0 in 1D / 2D).
+// kz = slab-axis index of q (plane in 3D, row in 2D; for the neighbour stores; 0 in 1D).
 template <int STAGE, typename T>
 __device__ __forceinline__ void rk_combine(const StageArgs<T> &A, int64_t q, int64_t kz, cplx<T> F, cplx<T> psi) {
     using C = cplx<T>;

@@ -50,7 +50,8 @@ diag_partial(const cplx<T> *__restrict__ Psi, const T *__restrict__ V, Grid g, d
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;
         }
-        if (DIM >= 2 && (row % g.ny) + 1 < g.ny) {
+        // y pairs (2D y-slabs: also across to the upper neighbour's first row, a ghost row)
+        if (DIM >= 2 && (row % g.ny) + 1 < g.ny + ((DIM == 2 && !g.zf_hi) ? 1 : 0)) {
             const cplx<T> u = Psi[q + g.sy];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;

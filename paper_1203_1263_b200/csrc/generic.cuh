@@ -26,14 +26,15 @@ struct PointEval {
 
     __device__ __forceinline__ int n_bnd(int64_t i, int64_t j, int64_t k) const {
         int m = (i == 0 || i == g.nx - 1);
-        if (DIM >= 2) m += (j == 0 || j == g.ny - 1);
+        if (DIM >= 2) m += y_face<DIM>(g, j);
         if (DIM >= 3) m += is_zface(g, k);
         return m;
     }
     // Inward neighbour: one step in along every boundary axis (R-MSD-NBR).
     __device__ __forceinline__ void inward(int64_t &i, int64_t &j, int64_t &k) const {
         i = (i == 0) ? 1 : (i == g.nx - 1 ? g.nx - 2 : i);
-        if (DIM >= 2) j = (j == 0) ? 1 : (j == g.ny - 1 ? g.ny - 2 : j);
+        if (DIM == 3) j = (j == 0) ? 1 : (j == g.ny - 1 ? g.ny - 2 : j);
+        if (DIM == 2) j = (g.zf_lo && j == 0) ? 1 : ((g.zf_hi && j == g.ny - 1) ? g.ny - 2 : j);
         if (DIM >= 3) k = (g.zf_lo && k == 0) ? 1 : ((g.zf_hi && k == g.nz - 1) ? g.nz - 2 : k);
     }
     __device__ __forceinline__ int64_t idx(int64_t i, int64_t j, int64_t k) const {
@@ -165,6 +166,10 @@ struct PointEval {
     }
 };
 
+// The slab-axis index of (j, k): the plane in 3D, the row in 2D (neighbour stores, store_out).
+template <int DIM>
+__device__ __forceinline__ int64_t slab_index(int64_t j, int64_t k) { return DIM == 3 ? k : (DIM == 2 ? j : 0); }
+
 // One thread per grid point over the whole grid.
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
@@ -177,11 +182,13 @@ __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_any(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, k, F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
 }
 
 // Boundary points only: a flat index over the boundary surface, mapped to (i,j,k).
-// 1D: 2 points; 2D: the 2(nx + ny) - 4 perimeter; 3D: the global z faces this grid
+// 1D: 2 points; 2D: the global y-face rows this slab owns (row 0 if zf_lo, row ny-1 if
+// zf_hi; both on one GPU), then the two x-face points of every other owned row (the
+// 2(nx + ny) - 4 perimeter on one GPU); 3D: the global z faces this grid
 // owns (plane 0 if zf_lo, plane nz-1 if zf_hi), then the perimeter of every other
 // owned plane.
 // rows_only (3D): the interior planes contribute their two y-face rows only (the x-face
@@ -205,8 +212,17 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
         else { const unsigned v = u - 2u * nx; ii = (v & 1u) ? nx - 1u : 0; jj = 1u + (v >> 1); }
     };
     if (DIM == 2) {
-        if (t >= per) return false;
-        perim(t, i, j); k = 0;
+        const unsigned nf = unsigned(g.zf_lo + g.zf_hi);
+        k = 0;
+        if (t < nf * nx) {
+            j = (g.zf_lo && t < nx) ? 0 : ny - 1u;
+            i = (t < nx) ? t : t - nx;
+            return true;
+        }
+        const unsigned v = t - nf * nx;
+        if (v >= 2u * (ny - nf)) return false;
+        i = (v & 1u) ? nx - 1u : 0;
+        j = unsigned(g.zf_lo) + (v >> 1);
         return true;
     }
     const unsigned face = nx * ny;
@@ -229,8 +245,8 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
 template <int DIM>
 inline int64_t n_boundary_points(const Grid &g, bool rows_only = false) {
     if (DIM == 1) return 2;
+    if (DIM == 2) return (g.zf_lo + g.zf_hi) * g.nx + 2 * (g.ny - g.zf_lo - g.zf_hi);
     const int64_t per = 2 * g.nx + (rows_only ? 0 : 2 * (g.ny - 2));
-    if (DIM == 2) return per;
     const int nf = g.zf_lo + g.zf_hi;
     return nf * g.nx * g.ny + per * (g.nz - nf);
 }
@@ -244,7 +260,7 @@ __global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_bnd(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, k, F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
 }
 
 // 3D MSD boundary points with F(b') taken from what the interior kernel stored (A.fz /
@@ -286,18 +302,19 @@ namespace nlse {
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(256) stage_interior_generic(StageArgs<T> A) {
     const int64_t k0 = DIM >= 3 ? A.g.zf_lo : 0;
-    const int64_t mx = A.g.nx - 2, my = DIM >= 2 ? A.g.ny - 2 : 1;
+    const int64_t j0 = DIM == 2 ? A.g.zf_lo : 1;                  // 2D: first owned interior row
+    const int64_t mx = A.g.nx - 2, my = DIM == 3 ? A.g.ny - 2 : (DIM == 2 ? A.g.ny - A.g.zf_lo - A.g.zf_hi : 1);
     const int64_t mz = DIM >= 3 ? A.g.nz - A.g.zf_lo - A.g.zf_hi : 1;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= mx * my * mz) return;
     const int64_t i = 1 + t % mx;
-    const int64_t j = DIM >= 2 ? 1 + (t / mx) % my : 0;
+    const int64_t j = DIM >= 2 ? j0 + (t / mx) % my : 0;
     const int64_t k = DIM >= 3 ? k0 + t / (mx * my) : 0;
     PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_int(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, k, F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
 }
 
 }  // namespace nlse

@@ -96,13 +96,18 @@ bool build_fused_maps(nlse_ctx *c) {
     const int eb = int(sizeof(T));
     bool ok = true;
     for (int b = 0; b < 4; b++) {
-        ok = ok && make_map(&c->fmaps.y[b], c->alloc[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
-        ok = ok && make_map(&c->fmaps.base[b], c->alloc[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_B_X, Cfg::BOX_B_Y);
+        ok = ok && make_map(&c->fmaps.y[b], c->buf[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
+        ok = ok && make_map(&c->fmaps.base[b], c->buf[b], eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_B_X, Cfg::BOX_B_Y);
     }
     ok = ok && make_map(&c->fmaps.k, c->K, eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_K_X, Cfg::BOX_K_Y);
     if (c->V) ok = ok && make_map(&c->fmaps.v, c->V, eb, nx, ny, nz, sy, Cfg::BOX_V_X, Cfg::BOX_V_Y);
     else c->fmaps.v = c->fmaps.k;   // never dereferenced without a V array
     return ok;
+}
+
+// First lower ghost plane of halo'd buffer b (the TMA maps address planes from there)
+void *ghost_base(const nlse_ctx *c, int b) {
+    return (char *)c->buf[b] - size_t(c->g.zghost) * size_t(c->g.su) * size_t(2 * c->eb);
 }
 
 template <typename T, int ORDER, int TYV>
@@ -112,8 +117,8 @@ bool build_maps(nlse_ctx *c) {
     const int eb = int(sizeof(T));
     bool ok = true;
     for (int b = 0; b < 3; b++)
-        ok = ok && make_map(&c->maps.y[b], c->alloc[b], eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
-    ok = ok && make_map(&c->maps.psi, c->alloc[BUF_PSI], eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_C_X, Cfg::BOX_O_Y);
+        ok = ok && make_map(&c->maps.y[b], ghost_base(c, b), eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_Y_X, Cfg::BOX_Y_Y);
+    ok = ok && make_map(&c->maps.psi, ghost_base(c, BUF_PSI), eb, 2 * nx, ny, nza, 2 * sy, Cfg::BOX_C_X, Cfg::BOX_O_Y);
     ok = ok && make_map(&c->maps.k, c->K, eb, 2 * nx, ny, nz, 2 * sy, Cfg::BOX_C_X, Cfg::BOX_O_Y);
     if (c->V) ok = ok && make_map(&c->maps.v, c->V, eb, nx, ny, nz, sy, Cfg::BOX_R_X, Cfg::BOX_O_Y);
     else c->maps.v = c->maps.k;   // never dereferenced without a V array
@@ -166,14 +171,14 @@ void enqueue_barrier(nlse_ctx *c, bool full, int mode = 3) {
 nlse_status enqueue_halo_refresh(nlse_ctx *c, int mode = 3) {
     if (!c->dist || !c->ghost_stale) return NLSE_OK;
     const int w = halo_w(c);
-    const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.sz) * cb;
+    const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.su) * cb;
     if (c->peer_alloc[BUF_PSI][0]) {
-        char *dst = (char *)c->peer_alloc[BUF_PSI][0] + (c->g.zghost + c->peer_nloc[0]) * plane;
+        char *dst = (char *)c->peer_alloc[BUF_PSI][0] + c->ghost_off + c->peer_nloc[0] * plane;
         CUDA_TRY(c, cudaMemcpyAsync(dst, c->buf[BUF_PSI], w * plane, cudaMemcpyDefault, c->stream));
     }
     if (c->peer_alloc[BUF_PSI][1]) {
-        char *dst = (char *)c->peer_alloc[BUF_PSI][1] + (c->g.zghost - w) * plane;
-        const char *src = (const char *)c->buf[BUF_PSI] + (c->g.nz - w) * plane;
+        char *dst = (char *)c->peer_alloc[BUF_PSI][1] + c->ghost_off - w * plane;
+        const char *src = (const char *)c->buf[BUF_PSI] + (c->g.ns - w) * plane;
         CUDA_TRY(c, cudaMemcpyAsync(dst, src, w * plane, cudaMemcpyDefault, c->stream));
     }
     enqueue_barrier(c, false, mode);
@@ -453,15 +458,18 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     if (dims[0] * dims[1] >= (int64_t(1) << 31) || dims[2] >= (int64_t(1) << 31))
         return fail(nullptr, NLSE_ERR_ARG, "an xy plane must have fewer than 2^31 points (32-bit in-plane indexing)");
     const int w = order == NLSE_2SHOC4 ? 2 : 1;
-    int64_t z0 = 0, nloc = dims[2];
+    // slab axis (§8(e)): z in 3D, y in 2D; nloc = its owned length
+    const int sax = ndim == 3 ? 2 : 1;
+    int64_t z0 = 0, nloc = dims[sax];
     if (dist) {
-        if (ndim != 3) return fail(nullptr, NLSE_ERR_ARG, "slab mode partitions 3D grids only (1D/2D run as replicas)");
+        if (ndim < 2) return fail(nullptr, NLSE_ERR_ARG, "slab mode partitions 2D (y rows) and 3D (z planes) grids; 1D grids run as replicas");
         if (nranks < 1 || nranks > NLSE_MAX_RANKS || rank < 0 || rank >= nranks)
             return fail(nullptr, NLSE_ERR_ARG, "rank / nranks out of range");
-        nlse_slab_range(dims[2], nranks, rank, &z0, &nloc);
-        if (nloc < 2 * w) return fail(nullptr, NLSE_ERR_ARG, "every slab needs at least 2w planes (w = 1 CD, 2 2SHOC)");
+        nlse_slab_range(dims[sax], nranks, rank, &z0, &nloc);
+        if (nloc < 2 * w) return fail(nullptr, NLSE_ERR_ARG, "every slab needs at least 2w planes / rows (w = 1 CD, 2 2SHOC)");
     }
-    const int64_t n = dims[0] * dims[1] * nloc;
+    const int64_t ny_own = ndim == 2 ? nloc : dims[1], nz_own = ndim == 3 ? nloc : 1;
+    const int64_t n = dims[0] * ny_own * nz_own;
     if (V) {
         for (int64_t q = 0; q < n; q++)
             if (!std::isfinite(V[q])) return fail(nullptr, NLSE_ERR_ARG, "V must be finite");
@@ -475,8 +483,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     for (int d = 0; d < 3; d++) c->dims[d] = dims[d];
     c->h = h; c->a = a; c->s = s; c->bc = bc; c->order = order; c->prec = prec; c->flags = flags;
     c->dist = dist; c->rank = rank; c->nranks = nranks; c->z0 = z0;
-    c->g.nx = dims[0]; c->g.ny = dims[1]; c->g.nz = nloc;
-    c->g.sy = dims[0]; c->g.sz = dims[0] * dims[1]; c->g.n = n;
+    c->g.nx = dims[0]; c->g.ny = ny_own; c->g.nz = nz_own;
+    c->g.sy = dims[0]; c->g.sz = dims[0] * ny_own; c->g.n = n;
     c->eb = prec == NLSE_FP64 ? 8 : 4;
     // Pitched rows: the 3D TMA kernels need 16-byte row strides in every array (complex rows
     // 2*nx*eb, V rows nx*eb bytes); the paper pads rows the same way (cudaMallocPitch).
@@ -494,6 +502,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->g.zf_lo = (!dist || rank == 0) ? 1 : 0;
     c->g.zf_hi = (!dist || rank == nranks - 1) ? 1 : 0;
     c->g.zghost = dist ? w : 0;
+    c->g.ns = ndim == 3 ? c->g.nz : (ndim == 2 ? c->g.ny : 1);
+    c->g.su = ndim == 2 ? c->g.sy : c->g.sz;
     c->hasV = V != nullptr;
     cudaGetDevice(&c->device);
     if (flags & NLSE_FLAG_GENERIC_KERNELS) c->interior_kind = KK_GENERIC;
@@ -518,13 +528,19 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         CREATE_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CREATE_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
-    const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.sz) * cb;
-    const size_t halo_bytes = (size_t(nloc) + 2 * size_t(c->g.zghost)) * plane;
-    const size_t cells = size_t(nloc) * size_t(c->g.sz);    // allocated points (>= n with pitched rows)
+    // one slab-axis unit (a plane in 3D, a row in 2D); the halo'd buffers carry zghost units of
+    // ghosts below and above the owned ones
+    const size_t cb = size_t(2 * c->eb), plane = size_t(c->g.su) * cb;
+    // the owned planes start 256-byte aligned (a row-sized 2D ghost unit need not be a 16-byte
+    // multiple); all ranks of a slab job use the same offset, so peers address each other's
+    // planes from their allocation bases
+    c->ghost_off = (size_t(c->g.zghost) * plane + 255) / 256 * 256;
+    const size_t halo_bytes = c->ghost_off + (size_t(c->g.ns) + size_t(c->g.zghost)) * plane;
+    const size_t cells = size_t(c->g.ns) * size_t(c->g.su);    // allocated points (>= n with pitched rows)
     for (int b = 0; b < 3; b++) {
         CREATE_TRY(cudaMalloc(&c->alloc[b], halo_bytes));
         CREATE_TRY(cudaMemsetAsync(c->alloc[b], 0, halo_bytes, c->stream));
-        c->buf[b] = (char *)c->alloc[b] + size_t(c->g.zghost) * plane;
+        c->buf[b] = (char *)c->alloc[b] + c->ghost_off;
     }
     CREATE_TRY(cudaMalloc(&c->K, cells * cb));
     CREATE_TRY(cudaMemsetAsync(c->K, 0, cells * cb, c->stream));
@@ -612,7 +628,7 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         if (ok && want_fused && order == NLSE_CD2 && !dist && (bc != NLSE_BC_MSD || c->fp)) {
             CREATE_TRY(cudaMalloc(&c->alloc[BUF_PSI2], halo_bytes));
             CREATE_TRY(cudaMemsetAsync(c->alloc[BUF_PSI2], 0, halo_bytes, c->stream));
-            c->buf[BUF_PSI2] = c->alloc[BUF_PSI2];
+            c->buf[BUF_PSI2] = (char *)c->alloc[BUF_PSI2] + c->ghost_off;
             c->device_bytes += int64_t(halo_bytes);
             const char *fty = getenv("NLSE_FUSED_TY");
             c->fused_ty = (fty && std::atoi(fty) == 8) ? 8 : 16;
@@ -735,7 +751,7 @@ nlse_status nlse_dist_export(nlse_ctx *c, void *handle) {
     if (!c->dist) return fail(c, NLSE_ERR_ARG, "not a slab-mode context");
     DistBlob b{};
     b.magic = kBlobMagic; b.version = NLSE_ABI_VERSION;
-    b.rank = c->rank; b.nranks = c->nranks; b.nloc = c->g.nz;
+    b.rank = c->rank; b.nranks = c->nranks; b.nloc = c->g.ns;
     b.pid = int32_t(getpid()); b.device = c->device;
     for (int i = 0; i < 3; i++) CUDA_TRY(c, cudaIpcGetMemHandle(&b.h[i], c->alloc[i]));
     CUDA_TRY(c, cudaIpcGetMemHandle(&b.h[3], c->comm));
@@ -800,7 +816,7 @@ nlse_status nlse_dist_connect_local(nlse_ctx *const *ctxs, int n) {
         for (int side = 0; side < 2; side++) {
             const int nb = side == 0 ? j - 1 : j + 1;
             if (nb < 0 || nb >= n) continue;
-            c->peer_nloc[side] = ctxs[nb]->g.nz;
+            c->peer_nloc[side] = ctxs[nb]->g.ns;
             for (int i = 0; i < 3; i++) c->peer_alloc[i][side] = ctxs[nb]->alloc[i];
         }
         c->connected = true;
@@ -1048,7 +1064,7 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     out->rank = c->rank;
     out->nranks = c->nranks;
     out->z0 = c->z0;
-    out->nz_local = c->g.nz;
+    out->nz_local = c->g.ns;
     return NLSE_OK;
 }
 

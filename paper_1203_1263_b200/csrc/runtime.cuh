@@ -62,6 +62,8 @@ struct nlse_ctx {
     int eb = 8;                      // sizeof(real)
     bool hasV = false;
     bool pitched = false;            // rows padded to g.sy > nx points (16-byte TMA strides)
+    size_t ghost_off = 0;            // bytes from a halo'd allocation to its plane / row 0 (>= the
+                                     // lower ghosts, rounded up to 256 B so that buf is aligned)
     // halo'd buffers: allocation base (plane -zghost) and plane-0 pointer
     void *alloc[4] = {nullptr, nullptr, nullptr, nullptr};
     void *buf[4] = {nullptr, nullptr, nullptr, nullptr};

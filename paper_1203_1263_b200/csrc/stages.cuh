@@ -137,9 +137,10 @@ template <typename T>
 void peer_ptrs(const nlse_ctx *c, int b, cplx<T> *&lo, cplx<T> *&hi) {
     lo = hi = nullptr;
     if (!c->dist || !c->connected) return;
-    const int64_t sz = c->g.sz, zg = c->g.zghost;
-    if (c->peer_alloc[b][0]) lo = (cplx<T> *)c->peer_alloc[b][0] + (zg + c->peer_nloc[0]) * sz;
-    if (c->peer_alloc[b][1]) hi = (cplx<T> *)c->peer_alloc[b][1] + (zg - c->g.nz) * sz;
+    const int64_t su = c->g.su;
+    // (the peer's plane / row 0 is ghost_off bytes into its allocation, as here)
+    if (c->peer_alloc[b][0]) lo = (cplx<T> *)((char *)c->peer_alloc[b][0] + c->ghost_off) + c->peer_nloc[0] * su;
+    if (c->peer_alloc[b][1]) hi = (cplx<T> *)((char *)c->peer_alloc[b][1] + c->ghost_off) - c->g.ns * su;
 }
 
 template <typename T, int DIM, int ORDER, int BC>

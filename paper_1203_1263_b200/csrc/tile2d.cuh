@@ -52,6 +52,11 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
     const int nx = int(A.g.nx), ny = int(A.g.ny);
     const int x0 = blockIdx.x * T2_TX, y0 = blockIdx.y * T2_TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    // y-slab mode (§8(e)): rows [ymlo, ymhi) are in memory (ghost rows of the neighbours below /
+    // above); rows [olo, ohi] are this slab's output rows; y faces only where the slab holds them
+    const bool flo = A.g.zf_lo != 0, fhi = A.g.zf_hi != 0;
+    const int ymlo = flo ? 0 : -A.g.zghost, ymhi = fhi ? ny : ny + A.g.zghost;
+    const int olo = flo ? 1 : 0, ohi = fhi ? ny - 2 : ny - 1;
 
     // (1) Y tile with halo (zero outside the grid; those values are never used), and Psi,
     // K_tot, V of the owned points, all as asynchronous copies
@@ -59,14 +64,14 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         const int gy = y0 + ly;
         for (int lx = tx - H; lx < T2_TX + H; lx += 32) {
             const int gx = x0 + lx;
-            const bool in = gx >= 0 && gx < nx && gy >= 0 && gy < ny;
+            const bool in = gx >= 0 && gx < nx && gy >= ymlo && gy < ymhi;
             t2_cp<int(sizeof(C))>(&ys[(ly + H) * PX + (lx + H)], A.Y + (in ? int64_t(gy) * A.g.sy + gx : 0), in);
         }
     }
 #pragma unroll
     for (int r = 0; r < T2_RPT; r++) {
         const int gx = x0 + tx, gy = y0 + ty + 8 * r;
-        if (gx >= 1 && gx <= nx - 2 && gy >= 1 && gy <= ny - 2) {
+        if (gx >= 1 && gx <= nx - 2 && gy >= olo && gy <= ohi) {
             const int64_t q = int64_t(gy) * A.g.sy + gx;
             if (STAGE != 1) {
                 t2_cp<int(sizeof(C))>(&ps[r * T2_NT + tid], A.Psi + q, true);
@@ -94,7 +99,8 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
 
     // (2) 2SHOC step 1 over the tile + ring.  Tiles whose ring is in-grid interior (the
     // bulk of a large grid) take the stencil everywhere, without per-point face tests.
-    const bool inner = x0 >= 2 && x0 + T2_TX <= nx - 2 && y0 >= 2 && y0 + T2_TY <= ny - 2;
+    const bool inner = x0 >= 2 && x0 + T2_TX <= nx - 2 && y0 - H >= ymlo && y0 + T2_TY + H <= ymhi &&
+                       (!flo || y0 >= 2) && (!fhi || y0 + T2_TY <= ny - 2);
     if (ORDER == ORDER_2SHOC && inner) {
         for (int e = tid; e < DPX * DPY; e += T2_NT) {
             const int lx = e % DPX - 1, ly = e / DPX - 1;
@@ -106,9 +112,12 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
             const int lx = e % DPX - 1, ly = e / DPX - 1;
             const int gx = x0 + lx, gy = y0 + ly;
             C d; d.x = T(NAN); d.y = T(NAN);
-            if (gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
-                const bool fx = (gx == 0 || gx == nx - 1), fy = (gy == 0 || gy == ny - 1);
-                if (!fx && !fy) {
+            // (ring points beyond the rows in memory or x faces of ghost rows are never used)
+            const bool ghost_row = gy < 0 || gy >= ny;
+            if (gx >= 0 && gx < nx && gy >= (flo ? 0 : ymlo + 1) && gy < (fhi ? ny : ymhi - 1)) {
+                const bool fx = (gx == 0 || gx == nx - 1), fy = (flo && gy == 0) || (fhi && gy == ny - 1);
+                if (fx && ghost_row) {
+                } else if (!fx && !fy) {
                     d = D_int(lx, ly);
                 } else if (BC == BC_L0 && !(fx && fy)) {
                     d.x = T(0); d.y = T(0);                       // (BCL0lap) P:352-355
@@ -143,7 +152,7 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
     for (int r = 0; r < T2_RPT; r++) {
         const int lx = tx, ly = ty + 8 * r;
         const int gx = x0 + lx, gy = y0 + ly;
-        if (gx < 1 || gx > nx - 2 || gy < 1 || gy > ny - 2) continue;
+        if (gx < 1 || gx > nx - 2 || gy < olo || gy > ohi) continue;
         const int64_t q = int64_t(gy) * A.g.sy + gx;
         const C yc = Ys(lx, ly);
         C L;
@@ -173,14 +182,14 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         // RK4 stage combine (RK4_GPU) P:495-519, as rk_combine with Psi, K_tot staged
         if (STAGE == 1) {
             A.K[q] = F;
-            store_out(A, q, 0, cfma(A.c.kc, F, yc));
+            store_out(A, q, gy, cfma(A.c.kc, F, yc));
         } else if (STAGE == 4) {
             const C o = cfma(A.c.kc, cadd(ks[r * T2_NT + tid], F), ps[r * T2_NT + tid]);
-            store_out(A, q, 0, o);
+            store_out(A, q, gy, o);
             if (!(isfinite(o.x) && isfinite(o.y))) atomicMin(A.diverged, *A.step_base + A.step);
         } else {
             A.K[q] = cfma(T(2), F, ks[r * T2_NT + tid]);
-            store_out(A, q, 0, cfma(A.c.kc, F, ps[r * T2_NT + tid]));
+            store_out(A, q, gy, cfma(A.c.kc, F, ps[r * T2_NT + tid]));
         }
     }
 }

@@ -28,14 +28,14 @@ def run_gpu(dims, h, psi0, k, nsteps, a=1.0, s=1.0, V=None, bc="dirichlet", sche
 
 def run_gpu_slabs(dims, h, psi0, k, nsteps, nranks, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc",
                   precision="fp64", generic=False, chunks=None, force_dt=True, diag=False):
-    """The same run as run_gpu, partitioned into `nranks` z slabs (virtual ranks on one GPU,
+    """The same run as run_gpu, partitioned into `nranks` z slabs (3D) or y-row slabs (2D) (virtual ranks on one GPU,
     nlse_dist_connect_local + nlse_step_group).  Returns the gathered global Psi (and the
     per-rank diagnostics after the run when diag=True)."""
     from paper_1203_1263_b200 import nlse
     svs = []
     try:
         for r in range(nranks):
-            z0, nl = nlse.nlse_slab_range(dims[2], nranks, r)
+            z0, nl = nlse.nlse_slab_range(dims[-1], nranks, r)
             Vl = None if V is None else np.ascontiguousarray(V[z0:z0 + nl])
             svs.append(nlse.Solver(dims, h, a=a, s=s, V=Vl, bc=bc, scheme=scheme, precision=precision,
                                    force_dt=force_dt, generic=generic, dist=(r, nranks)))

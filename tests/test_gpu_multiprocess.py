@@ -53,10 +53,11 @@ def _worker(rank, world, port, dims, h, k, nsteps, scheme, q):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world,scheme", [(2, "2shoc"), (3, "cd")])
-def test_multiprocess_slabs_bitwise(world, scheme):
-    dims, h, nsteps = (40, 24, 21), 0.5, 5
-    k = 0.5 * h * h / (3 * 2 ** 0.5) * (0.75 if scheme == "2shoc" else 1.0)
+@pytest.mark.parametrize("world,scheme,dims", [(2, "2shoc", (40, 24, 21)), (3, "cd", (40, 24, 21)),
+                                               (2, "2shoc", (70, 45)), (3, "cd", (50, 31))])
+def test_multiprocess_slabs_bitwise(world, scheme, dims):
+    h, nsteps = 0.5, 5
+    k = 0.5 * h * h / (len(dims) * 2 ** 0.5) * (0.75 if scheme == "2shoc" else 1.0)
     psi0 = case_input(dims, seed=77)
     one = run_gpu(dims, h, psi0, k, nsteps, s=-1.0, bc="msd", scheme=scheme)
     ctx = mp.get_context("spawn")

@@ -94,7 +94,10 @@ def test_slab_errors():
         Solver((20, 20, 7), 0.5, scheme="2shoc", dist=(1, 2))       # 4 + 3 planes: 3 < 2w
     assert e.value.status == NLSE_ERR_ARG
     with pytest.raises(NLSEError) as e:
-        Solver((20, 20), 0.5, dist=(0, 2))                          # 2D is not partitioned
+        Solver((200,), 0.5, dist=(0, 2))                            # 1D is not partitioned
+    assert e.value.status == NLSE_ERR_ARG
+    with pytest.raises(NLSEError) as e:
+        Solver((20, 7), 0.5, scheme="2shoc", dist=(1, 2))           # 2D: 4 + 3 rows: 3 < 2w
     assert e.value.status == NLSE_ERR_ARG
     sv = Solver((20, 20, 16), 0.5, dist=(1, 2))
     with pytest.raises(NLSEError) as e:
@@ -116,3 +119,43 @@ def test_virtual_group_requires_group_calls():
     finally:
         for sv in svs:
             sv.close()
+
+
+# ---------------------------------------------------------------------------------------------
+# 2D y-row slabs (§8(f) rank 4): rows are the slowest axis of a 2D grid, so a slab is a
+# contiguous block of rows with w ghost rows on each side, exactly as 3D z planes
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+def test_2d_slabs_bitwise_equal_single(scheme, bc, precision, withV, nranks):
+    dims = (133, 70)             # tiles of 32 x 16 with ragged tails; slabs cut tiles anywhere
+    h = 0.2
+    psi0 = case_input(dims, seed=51)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=52)) if withV else None
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    k = 0.5 * h * h / (2 * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
+    one = run_gpu(dims, h, psi0, k, 9, **kw)
+    many = run_gpu_slabs(dims, h, psi0, k, 9, nranks, **kw)
+    assert ulp_diff(many, one, precision) == 0
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_2d_slabs_match_oracle_chunks_thin_and_diagnostics(generic):
+    """2D slabs against the oracle (chunked calls, CUDA graphs not used by virtual groups),
+    slabs of exactly 2w rows and uneven splits, the generic kernels, global diagnostics."""
+    import oracle
+    h = 0.25
+    for dims, P, scheme in [((64, 48), 3, "2shoc"), ((40, 8), 2, "2shoc"), ((40, 13), 3, "2shoc"), ((37, 6), 3, "cd")]:
+        psi0 = case_input(dims, seed=53)
+        V = np.abs(inputs.random_smooth(dims, seed=54))
+        kw = dict(s=-1.0, V=V, bc="msd", scheme=scheme, generic=generic)
+        k = 0.5 * h * h / (2 * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
+        ref = run_oracle(dims, h, psi0, k, 10, s=-1.0, V=V, bc="msd", scheme=scheme)
+        out, (m, e) = run_gpu_slabs(dims, h, psi0, k, 10, P, chunks=[3, 1, 6], diag=True, **kw)
+        assert ulp_diff(out, ref, "fp64") == 0, (dims, P)
+        mo, eo = oracle.diagnostics(oracle.Problem(dims, h, a=1.0, s=-1.0, bc="msd"), out, V)
+        assert len(set(m)) == 1 and abs(m[0] - mo) <= 1e-12 * abs(mo) and abs(e[0] - eo) <= 1e-12 * abs(eo)
