@@ -54,7 +54,7 @@ def workload(name, rank=0, world=1):
     cfg["z0"], cfg["nloc"] = 0, (cfg["dims"][2] if len(cfg["dims"]) == 3 else 1)
     if world > 1:
         from paper_1203_1263_b200.nlse import nlse_slab_range
-        z0, nl = nlse_slab_range(cfg["dims"][2], world, rank)
+        z0, nl = nlse_slab_range(cfg["dims"][-1], world, rank)
         cfg["z0"], cfg["nloc"] = z0, nl
         if name.startswith("gpe3d"):
             n = cfg["dims"][0]
@@ -249,8 +249,9 @@ def config_block(cfg, args, replicas=False):
                         f"{'harmonic-trap V array' if cfg.get('has_V', cfg['V'] is not None) else 'V=0'} (BASELINE.json configs)",
             "grid": list(cfg["dims"]), "h": cfg["h"], "k": cfg["k"], "scheme": cfg["scheme"], "bc": cfg["bc"],
             "precision": cfg["precision"], "a": cfg["a"], "s": cfg["s"],
-            "parallelism": (f"{args.gpus} independent replicas (1D/2D grids are not partitioned)" if replicas
-                            else (f"z-slab x{args.gpus}" if args.gpus > 1 else "single GPU")),
+            "parallelism": (f"{args.gpus} independent replicas (1D and small 2D grids are not partitioned)" if replicas
+                            else ((f"{'z' if len(cfg['dims']) == 3 else 'y'}-slab x{args.gpus}") if args.gpus > 1
+                                  else "single GPU")),
             "l2": "inputs larger than L2 (no flush needed)" if int(np.prod(cfg["dims"])) * 64 > 2e9
                   else "working set L2-resident (L2-scale config, no flush)"}
 
@@ -278,9 +279,11 @@ def main():
     build.build()
     from paper_1203_1263_b200.nlse import Solver
 
-    # 1D / 2D grids are not partitioned: every rank runs its own
-    # replica of the whole grid (weak scaling); 3D grids are z-slab partitioned (strong scaling)
-    replicas = world > 1 and len(inputs_dims(args.config)) < 3
+    # 3D grids are z-slab partitioned and 2D grids of >= 4096^2 points y-slab partitioned (strong
+    # scaling); 1D grids and smaller 2D grids, whose per-GPU stage is shorter than a neighbour
+    # barrier, run one independent replica per rank (weak scaling)
+    dims_ = inputs_dims(args.config)
+    replicas = world > 1 and (len(dims_) == 1 or (len(dims_) == 2 and int(np.prod(dims_)) < 4096 * 4096))
     slab = world > 1 and not replicas
     cfg = workload(args.config, rank, world if slab else 1)
     if args.scheme:

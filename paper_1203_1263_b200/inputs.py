@@ -126,8 +126,9 @@ def config_dims(name: str):
     if name.startswith("dark1d"):
         h = float(name.split("_h")[1]) if "_h" in name else 0.1
         return (int(round(100.0 / h)) + 1,)
-    if name == "trap2d":
-        return (1024, 1024)
+    if name.startswith("trap2d"):
+        n = int(name.split("_")[1]) if "_" in name else 1024
+        return (n, n)
     if name in ("ring3d", "ring3d_fp32"):
         return (87, 87, 203)
     if name.startswith("gpe3d"):
@@ -151,10 +152,11 @@ def config(name: str):
         x = axis(n, h)
         return dict(name=name, dims=(n,), h=h, k=None, steps=None, a=1.0, s=-1.0, bc="msd",
                     scheme="2shoc", precision="fp64", psi0=dark_soliton(x), V=None)
-    if name == "trap2d":           # configs[2]
-        dims = (1024, 1024)
+    if name.startswith("trap2d"):  # configs[2]: trap2d (1024^2) or trap2d_<n> (n^2, same physical box / n)
+        n = int(name.split("_")[1]) if "_" in name else 1024
+        dims = (n, n)
         h = 0.25
-        V = harmonic_trap(dims, h, 1.0 / 256.0)
+        V = harmonic_trap(dims, h, 1.0 / 256.0 * (1024.0 / n))
         return dict(name=name, dims=dims, h=h, k=0.005, steps=1000, a=1.0, s=-1.0, bc="msd",
                     scheme="2shoc", precision="fp64", psi0=thomas_fermi(vortex2d(dims, h), V), V=V)
     if name in ("ring3d", "ring3d_fp32"):  # configs[3]
