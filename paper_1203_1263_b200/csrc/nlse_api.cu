@@ -1052,7 +1052,7 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     if (!out) return fail(c, NLSE_ERR_ARG, "out is NULL");
     memset(out, 0, sizeof *out);
     out->points = c->g.n;
-    int per_stage = c->interior_kind == KK_GENERIC ? 1 : 2;
+    int per_stage = (c->interior_kind == KK_GENERIC || c->interior_kind == KK_TILE1D) ? 1 : 2;
     if (c->dist && c->nranks > 1) per_stage += 1;
     out->launches_per_step = c->persist1d ? 0 : (c->fused ? 4 : 4 * per_stage);   // 0: one launch per nlse_step call
     const int64_t cbytes = 2 * c->eb, rv = c->hasV ? c->eb : 0;

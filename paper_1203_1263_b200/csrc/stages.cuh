@@ -118,6 +118,7 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
             launch_tile1d<T, ORDER, BC, STAGE>(A, c->stream);
         }
     }
+    if (DIM == 1) return;               // stage1d_tile finishes the two boundary points itself
     if (side) {
         cudaStreamWaitEvent(c->stream, c->ev_join, 0);
     } else if (DIM == 3 && BC == BC_MSD && A.fp) {

@@ -200,12 +200,139 @@ void launch_tile2d(const StageArgs<T> &A, cudaStream_t st) {
     stage2d_tile<T, ORDER, BC, STAGE><<<grid, T2_NT, 0, st>>>(A);
 }
 
-// 1D: interior points, one thread per point (the 1D configs are latency-bound: 1025-2001
-// points per stage).
+// 1D grids above the persistent single-CTA limit (the paper's Table 1 runs 1D up to 3e6 points,
+// P:664-686): one CTA per tile of T1_N = 256 x T1_R points.  The stage input Y is staged once
+// in shared memory with an H = w wide halo (coalesced loads), 2SHOC step 1 ((2shoc1d) P:197)
+// is evaluated once per tile point plus a one-point ring into a shared D tile (the face point
+// x = 0 / nx - 1 by the Laplacian form of the BC, (BCDlap) P:320-323, (BCMSDlap) P:336-344,
+// (BCL0lap) P:352-355), then step 2 ((2shoc1d2) P:198), F (fsplit) P:424-428 and the RK4 stage
+// combine (RK4_GPU) P:495-519 run per owned interior point with Psi, K_tot, V read once.
+// The two boundary points are finished by the CTAs owning their inward neighbours b' = 1 and
+// nx - 2 (F_b from F(b') in registers: (BCDdt) P:315-318, (msd) P:331-335, (BCL0dt) P:347-350),
+// so a stage is one launch.  DAG: DESIGN.md §3.1 (bitwise = oracle).
+constexpr int T1_NT = 256;
+
+// T1_R points per thread: 4 on long grids (fewer halo loads), 1 below 2^20 points (more CTAs
+// in flight: 1e4-1e5-point grids are latency-bound)
+template <typename T, int ORDER, int BC, int STAGE, int T1_R>
+__global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
+    using C = cplx<T>;
+    constexpr int T1_N = T1_NT * T1_R;
+    constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
+    __shared__ __align__(16) C ys[T1_N + 2 * H];
+    __shared__ __align__(16) C ds[(ORDER == ORDER_2SHOC) ? T1_N + 2 : 1];
+    const int64_t nx = A.g.nx;
+    const int64_t x0 = int64_t(blockIdx.x) * T1_N;
+    const int tid = threadIdx.x;
+    // (1) Y tile with halo (zero outside the grid: never used)
+    for (int e = tid; e < T1_N + 2 * H; e += T1_NT) {
+        const int64_t gx = x0 - H + e;
+        C v; v.x = T(0); v.y = T(0);
+        if (gx >= 0 && gx < nx) v = A.Y[gx];
+        ys[e] = v;
+    }
+    __syncthreads();
+    auto Yl = [&](int lx) -> C { return ys[lx + H]; };       // local x in [-H, T1_N + H)
+    auto d_int = [&](int lx) -> C {
+        const C yc = Yl(lx);
+        const C y2 = cadd(yc, yc);
+        return cscale(A.c.ih2, csub(cadd(Yl(lx - 1), Yl(lx + 1)), y2));
+    };
+    // (2) 2SHOC step 1 on the tile + one-point ring; faces by the Laplacian form of the BC
+    if (ORDER == ORDER_2SHOC) {
+        for (int e = tid; e < T1_N + 2; e += T1_NT) {
+            const int lx = e - 1;
+            const int64_t gx = x0 + lx;
+            C d; d.x = T(NAN); d.y = T(NAN);
+            if (gx > 0 && gx < nx - 1) {
+                d = d_int(lx);
+            } else if (gx == 0 || gx == nx - 1) {
+                if (BC == BC_L0) {
+                    d.x = T(0); d.y = T(0);
+                } else {
+                    const C yb = Yl(lx);
+                    T nb = A.c.s * ((yb.x * yb.x) + (yb.y * yb.y));
+                    if (A.V) nb = nb - __ldg(A.V + gx);
+                    if (BC == BC_DIRICHLET) {
+                        const T t = A.c.inv_a * nb;
+                        d.x = -(t * yb.x); d.y = -(t * yb.y);
+                    } else {
+                        const int lx1 = gx == 0 ? lx + 1 : lx - 1;
+                        const C y1 = Yl(lx1), d1 = d_int(lx1);
+                        const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+                        T re = T(0);
+                        if (!(rho1 < A.c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+                        T n1 = A.c.s * rho1;
+                        if (A.V) n1 = n1 - __ldg(A.V + (x0 + lx1));
+                        const T gg = re + ((n1 - nb) * A.c.inv_a);
+                        d = cscale(gg, yb);
+                    }
+                }
+            }
+            ds[e] = d;
+        }
+        __syncthreads();
+    }
+    // (3) step 2, F, RK4 stage combine at the owned interior points (coalesced: thread t owns
+    // points t, t + 256, ...)
+#pragma unroll
+    for (int r = 0; r < T1_R; r++) {
+        const int lx = tid + r * T1_NT;
+        const int64_t q = x0 + lx;
+        if (q < 1 || q > nx - 2) continue;
+        const C yc = Yl(lx);
+        C L;
+        if (ORDER == ORDER_CD) L = d_int(lx);
+        else L = cfma(A.c.c76, ds[lx + 1], cneg(cscale(A.c.c112, cadd(ds[lx], ds[lx + 2]))));
+        const T rho = (yc.x * yc.x) + (yc.y * yc.y);
+        const T sr = A.c.s * rho;
+        T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
+        T fi = tfma(A.c.a, L.x, sr * yc.x);
+        if (A.V) {
+            const T v = __ldg(A.V + q);
+            fr = tfma(v, yc.y, fr);
+            fi = tfma(-v, yc.x, fi);
+        }
+        C F; F.x = fr; F.y = fi;
+        const C psi = STAGE == 1 ? yc : A.Psi[q];
+        rk_combine<STAGE, T>(A, q, 0, F, psi);
+        // the boundary point whose b' is q (nx = 3: q = 1 is b' of both)
+        for (int side = 0; side < 2; side++) {
+            const int64_t qb = side == 0 ? 0 : nx - 1;
+            if (q != (side == 0 ? 1 : nx - 2)) continue;
+            const C yb = Yl(int(qb - x0));
+            C Fb;
+            if (BC == BC_DIRICHLET) {
+                Fb.x = T(0); Fb.y = T(0);
+            } else if (BC == BC_L0) {
+                const T rb = (yb.x * yb.x) + (yb.y * yb.y);
+                const T srb = A.c.s * rb;
+                T gr = tfma(-A.c.a, T(0), -(srb * yb.y));
+                T gi = tfma(A.c.a, T(0), srb * yb.x);
+                if (A.V) {
+                    const T vb = __ldg(A.V + qb);
+                    gr = tfma(vb, yb.y, gr);
+                    gi = tfma(-vb, yb.x, gi);
+                }
+                Fb.x = gr; Fb.y = gi;
+            } else {
+                T m = T(0);
+                if (!(rho < A.c.eps2)) m = ((F.y * yc.x) - (F.x * yc.y)) / rho;
+                Fb.x = -(m * yb.y);
+                Fb.y = m * yb.x;
+            }
+            const C psib = STAGE == 1 ? yb : A.Psi[qb];
+            rk_combine<STAGE, T>(A, qb, 0, Fb, psib);
+        }
+    }
+}
+
 template <typename T, int ORDER, int BC, int STAGE>
 void launch_tile1d(const StageArgs<T> &A, cudaStream_t st) {
-    const int64_t m = A.g.nx - 2;
-    stage_interior_generic<T, 1, ORDER, BC, STAGE><<<unsigned((m + 255) / 256), 256, 0, st>>>(A);
+    if (A.g.nx >= (int64_t(1) << 20))
+        stage1d_tile<T, ORDER, BC, STAGE, 4><<<unsigned((A.g.nx + 4 * T1_NT - 1) / (4 * T1_NT)), T1_NT, 0, st>>>(A);
+    else
+        stage1d_tile<T, ORDER, BC, STAGE, 1><<<unsigned((A.g.nx + T1_NT - 1) / T1_NT), T1_NT, 0, st>>>(A);
 }
 
 }  // namespace nlse

@@ -123,6 +123,8 @@ def config_dims(name: str):
     """The grid of a BASELINE configuration (as config(name)["dims"], without building its IC)."""
     if name == "bright1d":
         return (1025,)
+    if name.startswith("dark1d_n"):
+        return (int(name.split("_n")[1]),)
     if name.startswith("dark1d"):
         h = float(name.split("_h")[1]) if "_h" in name else 0.1
         return (int(round(100.0 / h)) + 1,)
@@ -146,6 +148,13 @@ def config(name: str):
         x = axis(1025, h)
         return dict(name=name, dims=dims, h=h, k=0.001, steps=1000, a=1.0, s=1.0, bc="dirichlet",
                     scheme="2shoc", precision="fp64", psi0=bright_soliton(x), V=None)
+    if name.startswith("dark1d_n"):  # configs[1] shape at N points on [-50, 50] (Table 1 sizes)
+        n = int(name.split("_n")[1])
+        h = 100.0 / (n - 1)
+        x = axis(n, h)
+        kb = 0.75 * h * h / 2 ** 0.5          # (stblin2shoc) P:368-372, 1D
+        return dict(name=name, dims=(n,), h=h, k=0.8 * kb, steps=None, a=1.0, s=-1.0, bc="msd",
+                    scheme="2shoc", precision="fp64", psi0=dark_soliton(x), V=None)
     if name.startswith("dark1d"):  # configs[1], e.g. dark1d_h0.1
         h = float(name.split("_h")[1]) if "_h" in name else 0.1
         n = int(round(100.0 / h)) + 1
