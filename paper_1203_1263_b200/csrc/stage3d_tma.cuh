@@ -570,6 +570,13 @@ __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
     return r;
 }
 
+#ifndef NLSE_PKV_EARLY
+#define NLSE_PKV_EARLY 1
+#endif
+#ifndef NLSE_HOIST
+#define NLSE_HOIST 1
+#endif
+
 // v2.3: the 2SHOC loop of t3_run for interior tiles (EDGE = false) with the per-plane
 // control work cut down (ncu source counters, r01 ncus: the v2.2 loop issued ~275 warp
 // instructions per point-stage, ~85 of them fp64): shared memory by 32-bit addresses from
@@ -808,9 +815,22 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         constexpr int I0 = PH, I1 = (PH + 1) % 3, I2 = (PH + 2) % 3;
         const bool zf1 = ZF && (z == zf1_at);
         const unsigned dB1 = (dB0 + DS == 4 * DS) ? 0u : dB0 + DS;
-        if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
+        // plane z+1 has been in shared memory since the previous plane: its loads go before the
+        // wait for plane z+2 (NLSE_HOIST >= 1), and with NLSE_HOIST >= 2 so do the plane-z loads
+        // of the edge cross terms
+#if NLSE_HOIST >= 1
         const C px1 = cadd(ldY(yB1, -1), ldY(yB1, 1));
         const C py1 = cadd(ldY(yB1, -PX), ldY(yB1, PX));
+#endif
+#if NLSE_HOIST >= 2
+        const C pxa = cadd(ldY(yB0, -PX - 1), ldY(yB0, -PX + 1));
+        const C pxb = cadd(ldY(yB0, PX - 1), ldY(yB0, PX + 1));
+#endif
+        if (!zf1) mbar_wait(bar0 + 8 * s2, par2);
+#if NLSE_HOIST < 1
+        const C px1 = cadd(ldY(yB1, -1), ldY(yB1, 1));
+        const C py1 = cadd(ldY(yB1, -PX), ldY(yB1, PX));
+#endif
         C yz2 = yq[I1], dn;
         if (zf1) {
             if (ok) dn = b.D_bc(int64_t(z + 1) * sz + qrow, yq[I1], int64_t(z) * sz + qrow, yq[I0], dq[I1]);
@@ -858,24 +878,39 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         mbar_arrive(cbar0 + 8 * ((j + 1) & 1));
         const C y2c = cadd(yq[I0], yq[I0]);
         const C y4 = cadd(y2c, y2c);
+#if NLSE_HOIST < 2
         const C pxa = cadd(ldY(yB0, -PX - 1), ldY(yB0, -PX + 1));
         const C pxb = cadd(ldY(yB0, PX - 1), ldY(yB0, PX + 1));
+#endif
         const C exy = csub(cadd(pxa, pxb), y4);
         const C exz = csub(cadd(pxq[I0], px1), y4);
         const C eyz = csub(cadd(pyq[I0], py1), y4);
         const C E = cadd(cadd(exy, exz), eyz);
-        mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
-        if (tx == 0 && ty == (rot ? ((j + 3) & (TY - 1)) : TY - 1)) {
-            issue_y(z + H + P);
-            issue_pkv(z + Cfg::PP);
-        }
         C psi, kt; T v;
+#if NLSE_PKV_EARLY
+        // Psi / K_tot / V of plane z do not depend on the CTA barrier: load them before it, so
+        // their shared-memory latency overlaps the barrier wait (the slot of plane z is refilled
+        // only two planes later, after every thread has passed the barrier of plane z + 2)
         if (pkv_bytes) mbar_wait(bar0 + 8 * (NS + ps), pp);
         if (STAGE != 1) {
             psi = lds_c(ownP + pB, T());
             kt = lds_c(ownP + pB + Cfg::OWN_C, T());
         }
         if (hasV) v = lds_r(ownV + pB, T());
+#endif
+        mbar_wait(cbar0 + 8 * (j & 1), unsigned(j >> 1) & 1u);
+        if (tx == 0 && ty == (rot ? ((j + 3) & (TY - 1)) : TY - 1)) {
+            issue_y(z + H + P);
+            issue_pkv(z + Cfg::PP);
+        }
+#if !NLSE_PKV_EARLY
+        if (pkv_bytes) mbar_wait(bar0 + 8 * (NS + ps), pp);
+        if (STAGE != 1) {
+            psi = lds_c(ownP + pB, T());
+            kt = lds_c(ownP + pB + Cfg::OWN_C, T());
+        }
+        if (hasV) v = lds_r(ownV + pB, T());
+#endif
         const unsigned ad = ownD + dB0;
         const C sd = cadd(cadd(cadd(lds_c(ad - CB, T()), lds_c(ad + CB, T())),
                                cadd(lds_c(ad - DPX * CB, T()), lds_c(ad + DPX * CB, T()))),
