@@ -1,14 +1,18 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / synccheck / initcheck on small cases of every kernel family.
-out=gpurun_out/sanitize; mkdir -p $out
+out=gpurun_out/${TAG:-sanitize}; mkdir -p $out
 python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 CASES=("70x37x29 2shoc msd fp64 V" "70x37x29 2shoc dirichlet fp32" "64x33x9 2shoc msd fp64 V" "65x33x9 2shoc msd fp64"
-       "40x26x22 2shoc l0 fp64" "40x26x22 cd dirichlet fp32" "70x41 2shoc msd fp64 V" "301 2shoc msd fp64")
+       "40x26x22 2shoc l0 fp64" "40x26x22 cd dirichlet fp32" "70x41 2shoc msd fp64 V" "301 2shoc msd fp64"
+       "6001 2shoc msd fp64 V" "6001 cd l0 fp32" "FUSED=1 70x37x29 cd msd fp64 V" "FUSED=1 33x17x9 cd dirichlet fp32"
+       "SLABS=3 133x70 2shoc msd fp64 V" "SLABS=3 40x26x22 2shoc msd fp32")
 for tool in memcheck racecheck synccheck initcheck; do
   # 70x37x29: interior (lean), lean edge and ragged tiles; 64x33x9 / 65x33x9: tiles whose ring holds a
   # face point (per-point face path); 40x26x22: all tiles on the lean edge path
   for c in "${CASES[@]}"; do
-    NSTEPS=2 timeout 300 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/debug_case.py $c > $out/${tool}_${c// /_}.log 2>&1
+    envs=""; args="$c"
+    case "$c" in FUSED=1*) envs="NLSE_FUSED=1"; args="${c#FUSED=1 }";; SLABS=*) envs="${c%% *}"; args="${c#* }";; esac
+    env NSTEPS=2 $envs timeout 300 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/debug_case.py $args > $out/${tool}_${c// /_}.log 2>&1
     rc=$?
     echo "$tool [$c] rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|Hazard' $out/${tool}_${c// /_}.log | head -2 | tr '\n' ' ')"
   done
