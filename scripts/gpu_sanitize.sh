@@ -6,7 +6,8 @@ CASES=("70x37x29 2shoc msd fp64 V" "70x37x29 2shoc dirichlet fp32" "64x33x9 2sho
        "40x26x22 2shoc l0 fp64" "40x26x22 cd dirichlet fp32" "70x41 2shoc msd fp64 V" "301 2shoc msd fp64"
        "6001 2shoc msd fp64 V" "6001 cd l0 fp32" "FUSED=1 70x37x29 cd msd fp64 V" "FUSED=1 33x17x9 cd dirichlet fp32"
        "SLABS=3 133x70 2shoc msd fp64 V" "SLABS=3 40x26x22 2shoc msd fp32")
-for tool in memcheck racecheck synccheck initcheck; do
+[ -n "$ONLY_NEW" ] && CASES=("${CASES[@]:8}")     # the round-2 kernels only
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   # 70x37x29: interior (lean), lean edge and ragged tiles; 64x33x9 / 65x33x9: tiles whose ring holds a
   # face point (per-point face path); 40x26x22: all tiles on the lean edge path
   for c in "${CASES[@]}"; do
