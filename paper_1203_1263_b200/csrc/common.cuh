@@ -35,6 +35,40 @@ template <typename C, typename T> __device__ __forceinline__ C cfma(T s, C a, C 
 }
 template <typename C> __device__ __forceinline__ C cneg(C a) { C r; r.x = -a.x; r.y = -a.y; return r; }
 
+// fp32: the componentwise complex operations as sm_100 packed-fp32 instructions (FADD2 / FMUL2 /
+// FFMA2: add / mul / fma .rn.f32x2).  Each lane is one IEEE round-to-nearest fp32 operation, no
+// FTZ, exactly as the scalar pair it replaces -- same bits, half the FP instructions (the fp32
+// stage kernels are bound by their instruction stream).  Non-template overloads: preferred over
+// the templates above for float2 arguments.
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    float2 r;
+    asm("{\n.reg .b64 ra, rb, rr;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nadd.rn.f32x2 rr, ra, rb;\n"
+        "mov.b64 {%0, %1}, rr;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    float2 r;
+    asm("{\n.reg .b64 ra, rb, rr;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nsub.rn.f32x2 rr, ra, rb;\n"
+        "mov.b64 {%0, %1}, rr;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+__device__ __forceinline__ float2 cscale(float s, float2 a) {
+    float2 r;
+    asm("{\n.reg .b64 rs, ra, rr;\nmov.b64 rs, {%2, %2};\nmov.b64 ra, {%3, %4};\nmul.rn.f32x2 rr, rs, ra;\n"
+        "mov.b64 {%0, %1}, rr;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(s), "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 cfma(float s, float2 a, float2 b) {
+    float2 r;
+    asm("{\n.reg .b64 rs, ra, rb, rr;\nmov.b64 rs, {%2, %2};\nmov.b64 ra, {%3, %4};\nmov.b64 rb, {%5, %6};\n"
+        "fma.rn.f32x2 rr, rs, ra, rb;\nmov.b64 {%0, %1}, rr;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(s), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
 // Per-run constants, evaluated in double on the host from the user's doubles and
 // rounded once to T (reading R-CONST).
 template <typename T> struct Consts {
