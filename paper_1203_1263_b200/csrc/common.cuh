@@ -69,6 +69,41 @@ __device__ __forceinline__ float2 cfma(float s, float2 a, float2 b) {
     return r;
 }
 
+// F (fsplit) P:424-428 at one point, split as the kernels evaluate it (R-ASSOC):
+//   f_lin:  (fma(-a, L_I, -(sr Y_I)), fma(a, L_R, sr Y_R))      sr = s |Y|^2
+//   f_addv: (fma(V, Y_I, F_R), fma(-V, Y_R, F_I))                 (with a V array)
+// fp32: one FMUL2 + one FFMA2 (lane swap and per-lane negation are operand modifiers), one
+// FFMA2 for the V term -- the same IEEE operations per lane as the scalar forms.
+template <typename T> __device__ __forceinline__ cplx<T> f_lin(T a, cplx<T> L, T sr, cplx<T> y) {
+    cplx<T> F;
+    F.x = tfma(-a, L.y, -(sr * y.y));
+    F.y = tfma(a, L.x, sr * y.x);
+    return F;
+}
+template <typename T> __device__ __forceinline__ cplx<T> f_addv(cplx<T> F, T v, cplx<T> y) {
+    cplx<T> r;
+    r.x = tfma(v, y.y, F.x);
+    r.y = tfma(-v, y.x, F.y);
+    return r;
+}
+__device__ __forceinline__ float2 f_lin(float a, float2 L, float sr, float2 y) {
+    float2 r;
+    asm("{\n.reg .b64 rs, ry, rt, ra, rl, rn;\n.reg .f32 t0, t1, n1, na;\n"
+        "mov.b64 rs, {%2, %2};\nmov.b64 ry, {%3, %4};\nmul.rn.f32x2 rt, rs, ry;\n"
+        "mov.b64 {t0, t1}, rt;\nneg.f32 n1, t1;\nmov.b64 rn, {n1, t0};\n"
+        "neg.f32 na, %7;\nmov.b64 ra, {na, %7};\nmov.b64 rl, {%6, %5};\n"
+        "fma.rn.f32x2 rt, ra, rl, rn;\nmov.b64 {%0, %1}, rt;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(sr), "f"(y.x), "f"(y.y), "f"(L.x), "f"(L.y), "f"(a));
+    return r;
+}
+__device__ __forceinline__ float2 f_addv(float2 F, float v, float2 y) {
+    float2 r;
+    asm("{\n.reg .b64 rv, ry, rf, rr;\n.reg .f32 nv;\nneg.f32 nv, %2;\nmov.b64 rv, {%2, nv};\n"
+        "mov.b64 ry, {%4, %3};\nmov.b64 rf, {%5, %6};\nfma.rn.f32x2 rr, rv, ry, rf;\nmov.b64 {%0, %1}, rr;\n}"
+        : "=f"(r.x), "=f"(r.y) : "f"(v), "f"(y.x), "f"(y.y), "f"(F.x), "f"(F.y));
+    return r;
+}
+
 // Per-run constants, evaluated in double on the host from the user's doubles and
 // rounded once to T (reading R-CONST).
 template <typename T> struct Consts {

@@ -184,10 +184,8 @@ fused3d_cd(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUten
     auto fsplit = [&](C y, C L, T v) -> C {
         const T rho = (y.x * y.x) + (y.y * y.y);
         const T sr = s_ * rho;
-        T fr = tfma(-a_, L.y, -(sr * y.y));
-        T fi = tfma(a_, L.x, sr * y.x);
-        if (hasV) { fr = tfma(v, y.y, fr); fi = tfma(-v, y.x, fi); }
-        C F; F.x = fr; F.y = fi;
+        C F = f_lin(a_, L, sr, y);
+        if (hasV) F = f_addv(F, v, y);
         return F;
     };
     // CD: L = D = (((Px - Y2) + (Py - Y2)) + (Pz - Y2)) * ih2 from a plane view with row pitch W

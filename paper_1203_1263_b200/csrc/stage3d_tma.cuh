@@ -231,10 +231,8 @@ __device__ __forceinline__ void t3_finish(const StageArgs<T> &A, const HotC<T> &
     using C = cplx<T>;
     const T rho = (yc.x * yc.x) + (yc.y * yc.y);
     const T sr = hc.s * rho;
-    T fr = tfma(-hc.a, L.y, -(sr * yc.y));
-    T fi = tfma(hc.a, L.x, sr * yc.x);
-    if (A.V) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
-    C F; F.x = fr; F.y = fi;
+    C F = f_lin(hc.a, L, sr, yc);
+    if (A.V) F = f_addv(F, v, yc);
     if (A.fp) {
         const int nx = int(A.g.nx), ny = int(A.g.ny), nz = int(A.g.nz);
         if (A.g.zf_lo && z == 1) A.fz[gy * nx + gx] = F;
@@ -921,10 +919,8 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
         const C yc = yq[I0];
         const T rho = (yc.x * yc.x) + (yc.y * yc.y);
         const T sr = hc.s * rho;
-        T fr = tfma(-hc.a, L.y, -(sr * yc.y));
-        T fi = tfma(hc.a, L.x, sr * yc.x);
-        if (hasV) { fr = tfma(v, yc.y, fr); fi = tfma(-v, yc.x, fi); }
-        C F; F.x = fr; F.y = fi;
+        C F = f_lin(hc.a, L, sr, yc);
+        if (hasV) F = f_addv(F, v, yc);
         if (shell) A.fp[int64_t(z) * A.per2 + shell_i] = F;
         if (ok && (z == fz_lo || z == fz_hi)) {
             if (z == fz_lo) A.fz[gy * nx + gx] = F;

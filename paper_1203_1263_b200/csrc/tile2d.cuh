@@ -171,14 +171,8 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
         // F (fsplit) P:424-428
         const T rho = (yc.x * yc.x) + (yc.y * yc.y);
         const T sr = A.c.s * rho;
-        T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
-        T fi = tfma(A.c.a, L.x, sr * yc.x);
-        if (A.V) {
-            const T v = vs[r * T2_NT + tid];
-            fr = tfma(v, yc.y, fr);
-            fi = tfma(-v, yc.x, fi);
-        }
-        C F; F.x = fr; F.y = fi;
+        C F = f_lin(A.c.a, L, sr, yc);
+        if (A.V) F = f_addv(F, vs[r * T2_NT + tid], yc);
         // RK4 stage combine (RK4_GPU) P:495-519, as rk_combine with Psi, K_tot staged
         if (STAGE == 1) {
             A.K[q] = F;
@@ -286,14 +280,8 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
         else L = cfma(A.c.c76, ds[lx + 1], cneg(cscale(A.c.c112, cadd(ds[lx], ds[lx + 2]))));
         const T rho = (yc.x * yc.x) + (yc.y * yc.y);
         const T sr = A.c.s * rho;
-        T fr = tfma(-A.c.a, L.y, -(sr * yc.y));
-        T fi = tfma(A.c.a, L.x, sr * yc.x);
-        if (A.V) {
-            const T v = __ldg(A.V + q);
-            fr = tfma(v, yc.y, fr);
-            fi = tfma(-v, yc.x, fi);
-        }
-        C F; F.x = fr; F.y = fi;
+        C F = f_lin(A.c.a, L, sr, yc);
+        if (A.V) F = f_addv(F, __ldg(A.V + q), yc);
         const C psi = STAGE == 1 ? yc : A.Psi[q];
         rk_combine<STAGE, T>(A, q, 0, F, psi);
         // the boundary point whose b' is q (nx = 3: q = 1 is b' of both)
