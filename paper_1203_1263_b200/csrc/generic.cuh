@@ -243,7 +243,7 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
 }
 
 template <int DIM>
-inline int64_t n_boundary_points(const Grid &g, bool rows_only = false) {
+__host__ __device__ inline int64_t n_boundary_points(const Grid &g, bool rows_only = false) {
     if (DIM == 1) return 2;
     if (DIM == 2) return (g.zf_lo + g.zf_hi) * g.nx + 2 * (g.ny - g.zf_lo - g.zf_hi);
     const int64_t per = 2 * g.nx + (rows_only ? 0 : 2 * (g.ny - 2));

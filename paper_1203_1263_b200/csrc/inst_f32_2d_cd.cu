@@ -3,3 +3,4 @@
 #include "stages.cuh"
 
 NLSE_DEFINE_STAGES(f32, 2, cd)
+NLSE_DEFINE_PERSIST2D(f32, cd)

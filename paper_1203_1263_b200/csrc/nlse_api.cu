@@ -640,6 +640,22 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
             c->fused = fok;
         }
     }
+    // 2D: all stages of an nlse_step call in one cooperative launch (tile2d.cuh rk4_2d_persistent)
+    if (ndim == 2 && !dist && c->interior_kind == KK_TILE2D) {
+        const char *ep = getenv("NLSE_PERSIST2D");
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device);
+        // measured slower than the per-stage kernels (1024^2: 115.7 vs 77.8 us/step, r02r: tiles run
+        // one after another inside a CTA and 4 grid barriers per step serialise ~600 CTAs), so off
+        // by default; NLSE_PERSIST2D=1 selects it
+        const bool want = ep && ep[0] == '1';
+        if (want && coop) {
+            CREATE_TRY(cudaMalloc(&c->d_bar, 2 * sizeof(unsigned)));
+            CREATE_TRY(cudaMemsetAsync(c->d_bar, 0, 2 * sizeof(unsigned), c->stream));
+            CREATE_TRY(cudaStreamSynchronize(c->stream));
+            c->persist2d = true;
+        }
+    }
 #undef CREATE_TRY
     c->persist1d = use_persist1d(c);
     c->connected = !dist;
@@ -654,6 +670,14 @@ nlse_status enqueue_steps(nlse_ctx *c, double k, int64_t nsteps) {
         const bool f64 = c->prec == NLSE_FP64, shoc = c->order == NLSE_2SHOC4;
         (f64 ? (shoc ? persist1d_f64_shoc : persist1d_f64_cd) : (shoc ? persist1d_f32_shoc : persist1d_f32_cd))(
             c, k, nsteps);
+        enqueue_add_steps(c, nsteps);
+        return NLSE_OK;
+    }
+    if (c->persist2d) {
+        const bool f64 = c->prec == NLSE_FP64, shoc = c->order == NLSE_2SHOC4;
+        (f64 ? (shoc ? persist2d_f64_shoc : persist2d_f64_cd) : (shoc ? persist2d_f32_shoc : persist2d_f32_cd))(
+            c, k, nsteps);
+        CUDA_TRY(c, cudaGetLastError());
         enqueue_add_steps(c, nsteps);
         return NLSE_OK;
     }
@@ -719,7 +743,7 @@ void nlse_destroy(nlse_ctx *c) {
     for (int b = 0; b < 4; b++) cudaFree(c->alloc[b]);
     cudaFree(c->K); cudaFree(c->V); cudaFree(c->comm); cudaFree(c->fz); cudaFree(c->fp);
     drop_graph(c);
-    cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result);
+    cudaFree(c->d_div); cudaFree(c->d_steps); cudaFree(c->d_partial); cudaFree(c->d_result); cudaFree(c->d_bar);
     if (c->h_div) cudaFreeHost(c->h_div);
     if (c->h_result) cudaFreeHost(c->h_result);
     if (c->side_stream) { cudaStreamSynchronize(c->side_stream); cudaStreamDestroy(c->side_stream); }
@@ -1054,13 +1078,15 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     out->points = c->g.n;
     int per_stage = (c->interior_kind == KK_GENERIC || c->interior_kind == KK_TILE1D) ? 1 : 2;
     if (c->dist && c->nranks > 1) per_stage += 1;
-    out->launches_per_step = c->persist1d ? 0 : (c->fused ? 4 : 4 * per_stage);   // 0: one launch per nlse_step call
+    out->launches_per_step = (c->persist1d || c->persist2d) ? 0 : (c->fused ? 4 : 4 * per_stage);   // 0: one launch per nlse_step call
     const int64_t cbytes = 2 * c->eb, rv = c->hasV ? c->eb : 0;
     out->min_bytes_per_step = (16 * cbytes + 4 * rv) * c->g.n;
     out->device_bytes = c->device_bytes;
     out->elem_bytes = c->eb;
     snprintf(out->variant, sizeof out->variant, "%s",
-             c->persist1d ? "rk4_1d_persistent" : (c->fused ? kKindName[KK_FUSED3D] : kKindName[c->interior_kind]));
+             c->persist1d ? "rk4_1d_persistent"
+                          : (c->persist2d ? "rk4_2d_persistent"
+                                          : (c->fused ? kKindName[KK_FUSED3D] : kKindName[c->interior_kind])));
     out->rank = c->rank;
     out->nranks = c->nranks;
     out->z0 = c->z0;

@@ -123,6 +123,8 @@ struct nlse_ctx {
     bool ghost_stale = false;
     bool virtual_group = false;      // connected by nlse_dist_connect_local: _group calls only
     bool persist1d = false;          // 1D: one persistent CTA per nlse_step call
+    bool persist2d = false;          // 2D L2-scale grids: one cooperative launch per nlse_step call
+    unsigned *d_bar = nullptr;       // its grid barrier (count, generation)
 };
 
 namespace nlse_rt {
@@ -245,6 +247,10 @@ inline void swap_psi(nlse_ctx *c) {
     void enqueue_stage_##P##_##D##d_##O##_l0(nlse_ctx *, int, double, int);
 NLSE_FAMILIES(NLSE_DECLARE_FAMILY)
 #undef NLSE_DECLARE_FAMILY
+void persist2d_f64_cd(nlse_ctx *, double, int64_t);
+void persist2d_f64_shoc(nlse_ctx *, double, int64_t);
+void persist2d_f32_cd(nlse_ctx *, double, int64_t);
+void persist2d_f32_shoc(nlse_ctx *, double, int64_t);
 void persist1d_f64_cd(nlse_ctx *, double, int64_t);
 void persist1d_f64_shoc(nlse_ctx *, double, int64_t);
 void persist1d_f32_cd(nlse_ctx *, double, int64_t);

@@ -289,6 +289,50 @@ void fused_step_t(nlse_ctx *c, double k, int step) {
     swap_psi(c);
 }
 
+// 2D L2-scale grids: every stage of nsteps steps in one cooperative launch (tile2d.cuh).
+template <typename T, int ORDER, int BC>
+void launch_persist2d(nlse_ctx *c, double k, int64_t nsteps) {
+    using C = cplx<T>;
+    Persist2DArgs<T> P{};
+    for (int s = 1; s <= 4; s++) {
+        StageArgs<T> &A = P.A[s - 1];
+        const double kc = s == 3 ? k : (s == 4 ? k / 6.0 : k / 2.0);
+        A.Y = (const C *)c->buf[ybuf_of_stage(s)];
+        A.Psi = (const C *)c->buf[BUF_PSI];
+        A.K = (C *)c->K;
+        A.out = (C *)c->buf[obuf_of_stage(s)];
+        A.V = (const T *)c->V;
+        A.g = c->g;
+        A.c = make_consts<T>(c, kc);
+        A.diverged = c->d_div;
+        A.step_base = c->d_steps;
+        A.wsend = halo_w(c);
+    }
+    P.nsteps = nsteps;
+    P.bar_count = c->d_bar;
+    P.bar_gen = c->d_bar + 1;
+    auto kern = rk4_2d_persistent<T, ORDER, BC>;
+    static PerDevice per_sm_cache;
+    int per_sm = per_sm_cache.get(c->device);
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T2_NT, 0);
+        if (per_sm < 1) per_sm = 1;
+        per_sm_cache.set(c->device, per_sm);
+    }
+    const int64_t ntiles = ((c->g.nx + T2_TX - 1) / T2_TX) * ((c->g.ny + T2_TY - 1) / T2_TY);
+    const unsigned grid = unsigned(std::min<int64_t>(ntiles, int64_t(c->nsm) * per_sm));
+    void *args[] = {&P};
+    LaunchTimer lt(c, KK_TILE2D, c->g.n * nsteps * 4);
+    cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(T2_NT), args, 0, c->stream);
+}
+
+template <typename T, int ORDER>
+void persist2d_family(nlse_ctx *c, double k, int64_t nsteps) {
+    if (c->bc == NLSE_BC_MSD) launch_persist2d<T, ORDER, BC_MSD>(c, k, nsteps);
+    else if (c->bc == NLSE_BC_L0) launch_persist2d<T, ORDER, BC_L0>(c, k, nsteps);
+    else launch_persist2d<T, ORDER, BC_DIRICHLET>(c, k, nsteps);
+}
+
 template <typename T, int ORDER>
 void persist1d_family(nlse_ctx *c, double k, int64_t nsteps) {
     if (c->bc == NLSE_BC_MSD) launch_persist1d<T, ORDER, BC_MSD>(c, k, nsteps);
@@ -315,6 +359,10 @@ void persist1d_family(nlse_ctx *c, double k, int64_t nsteps) {
 #define NLSE_DEFINE_PERSIST1D(P, O)                                                             \
     void nlse_rt::persist1d_##P##_##O(nlse_ctx *c, double k, int64_t nsteps) {                  \
         nlse_rt::persist1d_family<NLSE_REAL_##P, NLSE_ORDER_##O>(c, k, nsteps);                 \
+    }
+#define NLSE_DEFINE_PERSIST2D(P, O)                                                             \
+    void nlse_rt::persist2d_##P##_##O(nlse_ctx *c, double k, int64_t nsteps) {                  \
+        nlse_rt::persist2d_family<NLSE_REAL_##P, NLSE_ORDER_##O>(c, k, nsteps);                 \
     }
 #define NLSE_DEFINE_FUSED(P, B)                                                                 \
     void nlse_rt::fused_step_##P##_##B(nlse_ctx *c, double k, int step) {                       \

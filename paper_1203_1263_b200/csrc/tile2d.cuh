@@ -39,18 +39,29 @@ __device__ __forceinline__ void t2_cp_wait_all() {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-template <typename T, int ORDER, int BC, int STAGE>
-__global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
+// Shared memory of one 2D tile (sized for stages 2-4; stage 1 leaves Psi / K_tot unused).
+template <typename T, int ORDER>
+struct T2Smem {
     using C = cplx<T>;
-    constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
-    constexpr int PX = T2_TX + 2 * H, PY = T2_TY + 2 * H;
-    constexpr int DPX = T2_TX + 2, DPY = T2_TY + 2;
-    __shared__ __align__(16) C ys[PY * PX];
-    __shared__ __align__(16) C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
-    __shared__ __align__(16) C ps[STAGE != 1 ? T2_RPT * T2_NT : 1], ks[STAGE != 1 ? T2_RPT * T2_NT : 1];
-    __shared__ __align__(16) T vs[T2_RPT * T2_NT];
+    static constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
+    static constexpr int PX = T2_TX + 2 * H, PY = T2_TY + 2 * H;
+    static constexpr int DPX = T2_TX + 2, DPY = T2_TY + 2;
+    C ys[PY * PX];
+    C ds[(ORDER == ORDER_2SHOC) ? DPY * DPX : 1];
+    C ps[T2_RPT * T2_NT], ks[T2_RPT * T2_NT];
+    T vs[T2_RPT * T2_NT];
+};
+
+// One 32 x T2_TY tile at (x0, y0) of one stage (the whole body of stage2d_tile; the persistent
+// 2D kernel runs it for many tiles and stages).
+template <typename T, int ORDER, int BC, int STAGE>
+__device__ __forceinline__ void t2_tile(const StageArgs<T> &A, T2Smem<T, ORDER> &S, int x0, int y0) {
+    using C = cplx<T>;
+    constexpr int H = T2Smem<T, ORDER>::H, PX = T2Smem<T, ORDER>::PX;
+    constexpr int DPX = T2Smem<T, ORDER>::DPX, DPY = T2Smem<T, ORDER>::DPY;
+    C *ys = S.ys, *ds = S.ds, *ps = S.ps, *ks = S.ks;
+    T *vs = S.vs;
     const int nx = int(A.g.nx), ny = int(A.g.ny);
-    const int x0 = blockIdx.x * T2_TX, y0 = blockIdx.y * T2_TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     // y-slab mode (§8(e)): rows [ymlo, ymhi) are in memory (ghost rows of the neighbours below /
     // above); rows [olo, ohi] are this slab's output rows; y faces only where the slab holds them
@@ -185,6 +196,87 @@ __global__ void __launch_bounds__(T2_NT) stage2d_tile(StageArgs<T> A) {
             A.K[q] = cfma(T(2), F, ks[r * T2_NT + tid]);
             store_out(A, q, gy, cfma(A.c.kc, F, ps[r * T2_NT + tid]));
         }
+    }
+}
+
+#ifndef NLSE_T2_MINB
+#define NLSE_T2_MINB 1
+#endif
+template <typename T, int ORDER, int BC, int STAGE>
+__global__ void __launch_bounds__(T2_NT, NLSE_T2_MINB) stage2d_tile(StageArgs<T> A) {
+    __shared__ __align__(16) T2Smem<T, ORDER> S;
+    t2_tile<T, ORDER, BC, STAGE>(A, S, int(blockIdx.x) * T2_TX, int(blockIdx.y) * T2_TY);
+}
+
+// ------------------------------------------------------------------ persistent 2D stepper
+// L2-scale 2D grids (configs[2], 1024^2: ~1 M points, a stage is ~20 us of launch-bound work)
+// run every stage of every step of an nlse_step call in ONE cooperative launch: the co-resident
+// CTAs loop over the tiles of a stage (t2_tile) and over its boundary points (F by the BC
+// time-derivative form, as stage_boundary), then meet at a grid-wide barrier before the next
+// stage reads what this one wrote.  Same per-point operations as the per-stage kernels.
+template <typename T>
+struct Persist2DArgs {
+    StageArgs<T> A[4];           // stage operands (stage s + 1), step field set per step
+    int64_t nsteps;
+    unsigned *bar_count;         // grid barrier: arrivals of the current generation
+    unsigned *bar_gen;           // grid barrier: generation
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Sense-counting grid barrier over the co-resident CTAs of a cooperative launch.
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire_gpu_u32(gen);
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0;
+            __threadfence();
+            st_release_gpu_u32(gen, g + 1);
+        } else {
+            while (ld_acquire_gpu_u32(gen) == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T, int ORDER, int BC, int STAGE>
+__device__ __forceinline__ void p2_stage(const StageArgs<T> &A, T2Smem<T, ORDER> &S, int ntx, int ntiles) {
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        t2_tile<T, ORDER, BC, STAGE>(A, S, (t % ntx) * T2_TX, (t / ntx) * T2_TY);
+        __syncthreads();                 // the tile's shared arrays are reused by the next tile
+    }
+    const int64_t nb = n_boundary_points<2>(A.g);
+    PointEval<T, 2, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i, j, k;
+        bnd_point<2>(A.g, b, i, j, k);
+        const int64_t q = ev.idx(i, j, k);
+        const cplx<T> F = ev.F_bnd(i, j, k);
+        const cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
+        rk_combine<STAGE, T>(A, q, j, F, psi);
+    }
+}
+
+template <typename T, int ORDER, int BC>
+__global__ void __launch_bounds__(T2_NT) rk4_2d_persistent(const __grid_constant__ Persist2DArgs<T> P) {
+    __shared__ __align__(16) T2Smem<T, ORDER> S;
+    const int ntx = int((P.A[0].g.nx + T2_TX - 1) / T2_TX), nty = int((P.A[0].g.ny + T2_TY - 1) / T2_TY);
+    const int ntiles = ntx * nty;
+    for (int64_t n = 0; n < P.nsteps; n++) {
+        StageArgs<T> A;
+        A = P.A[0]; A.step = int(n); p2_stage<T, ORDER, BC, 1>(A, S, ntx, ntiles); grid_barrier(P.bar_count, P.bar_gen);
+        A = P.A[1]; A.step = int(n); p2_stage<T, ORDER, BC, 2>(A, S, ntx, ntiles); grid_barrier(P.bar_count, P.bar_gen);
+        A = P.A[2]; A.step = int(n); p2_stage<T, ORDER, BC, 3>(A, S, ntx, ntiles); grid_barrier(P.bar_count, P.bar_gen);
+        A = P.A[3]; A.step = int(n); p2_stage<T, ORDER, BC, 4>(A, S, ntx, ntiles); grid_barrier(P.bar_count, P.bar_gen);
     }
 }
 

@@ -118,3 +118,23 @@ def test_full_step_counts_match_oracle_digest(name):
     h = hashlib.sha256(np.ascontiguousarray(got.astype(dt)).tobytes()).hexdigest()
     assert np.all(np.isfinite(got)) and g["finite"]
     assert h == g["sha256"], (name, float(np.abs(got).max()), g["max_abs"])
+
+
+@pytest.mark.parametrize("persist", ["1", "0"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+def test_2d_persistent_and_per_stage_bitwise(scheme, bc, precision, persist, monkeypatch):
+    """2D grids up to 2^21 points run every stage of an nlse_step call in one cooperative launch
+    (rk4_2d_persistent: grid-wide barriers between stages); NLSE_PERSIST2D=0 forces the per-stage
+    kernels.  Both bit for bit against the oracle, chunked calls included."""
+    monkeypatch.setenv("NLSE_PERSIST2D", persist)
+    dims, h = (133, 70), 0.2
+    psi0 = case_input(dims, seed=61)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=62))
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    k = _k(2, h, scheme)
+    ref = run_oracle(dims, h, psi0, k, 19, **kw)
+    got, info = run_gpu(dims, h, psi0, k, 19, chunks=[1, 17, 1], with_info=True, **kw)
+    assert info["variant"] == ("rk4_2d_persistent" if persist == "1" else "stage2d_tile"), info
+    assert_parity(got, ref, precision, what=f"2D persist={persist} {scheme} {bc} {precision}")
