@@ -109,3 +109,21 @@ def test_no_cpu_fallback(nlse):
 def test_status_strings(nlse):
     assert nlse.lib.nlse_status_string(6) == b"NLSE_ERR_DIVERGED"
     assert nlse.lib.nlse_stability_bound(1, 1.0, 0.1, 3, None, None) == nlse.NLSE_ERR_ARG
+
+
+def build_c_demo(tmp_path):
+    """Compile tests/c/abi_demo.c as plain C against include/nlse.h and link libnlse_b200.so."""
+    import subprocess
+    from paper_1203_1263_b200 import build
+    build.build()
+    exe = str(tmp_path / "abi_demo")
+    libdir = os.path.dirname(build.LIB)
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-O2", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_demo.c"), "-o", exe, "-L", libdir, "-lnlse_b200",
+                           "-Wl,-rpath," + libdir, "-lm"])
+    return exe
+
+
+def test_c_client_compiles_and_links(tmp_path):
+    """The header is plain C (no torch / CUDA types) and a C program links every call it makes."""
+    assert os.path.exists(build_c_demo(tmp_path))

@@ -138,3 +138,24 @@ def test_2d_persistent_and_per_stage_bitwise(scheme, bc, precision, persist, mon
     got, info = run_gpu(dims, h, psi0, k, 19, chunks=[1, 17, 1], with_info=True, **kw)
     assert info["variant"] == ("rk4_2d_persistent" if persist == "1" else "stage2d_tile"), info
     assert_parity(got, ref, precision, what=f"2D persist={persist} {scheme} {bc} {precision}")
+
+
+def test_c_client_matches_oracle(tmp_path):
+    """A plain C client of include/nlse.h (tests/c/abi_demo.c: create, set_psi, step, get_psi,
+    diagnostics, destroy) returns the oracle's field bit for bit: the C ABI is the product
+    boundary, the ctypes binding only marshals arguments."""
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_abi import build_c_demo
+    exe = build_c_demo(tmp_path)
+    dims, nsteps = (37, 21, 19), 7
+    psi0 = case_input(dims, seed=71)
+    fin, fout = str(tmp_path / "in.bin"), str(tmp_path / "out.bin")
+    np.ascontiguousarray(psi0, np.complex128).tofile(fin)
+    res = subprocess.run([exe, *map(str, dims), str(nsteps), fin, fout], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    got = np.fromfile(fout, dtype=np.complex128).reshape(tuple(reversed(dims)))
+    k = float(res.stdout.split()[1])
+    ref = run_oracle(dims, 0.5, psi0, k, nsteps, a=1.0, s=-1.0, bc="msd", scheme="2shoc")
+    assert_parity(got, ref, "fp64", what="C client")
