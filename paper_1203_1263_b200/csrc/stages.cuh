@@ -322,6 +322,8 @@ void launch_persist2d(nlse_ctx *c, double k, int64_t nsteps) {
     const int64_t ntiles = ((c->g.nx + T2_TX - 1) / T2_TX) * ((c->g.ny + T2_TY - 1) / T2_TY);
     const unsigned grid = unsigned(std::min<int64_t>(ntiles, int64_t(c->nsm) * per_sm));
     void *args[] = {&P};
+    // a fresh barrier per launch (an aborted earlier launch cannot leave it mid-generation)
+    cudaMemsetAsync(c->d_bar, 0, 2 * sizeof(unsigned), c->stream);
     LaunchTimer lt(c, KK_TILE2D, c->g.n * nsteps * 4);
     cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(T2_NT), args, 0, c->stream);
 }
