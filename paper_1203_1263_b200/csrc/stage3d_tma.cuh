@@ -118,7 +118,10 @@ struct T3Cfg {
 #ifndef NLSE_TMA_PP64
 #define NLSE_TMA_PP64 3
 #endif
-    static constexpr int PP = (sizeof(T) == 8) ? NLSE_TMA_PP64 : 3;
+#ifndef NLSE_TMA_PP32
+#define NLSE_TMA_PP32 3
+#endif
+    static constexpr int PP = (sizeof(T) == 8) ? NLSE_TMA_PP64 : NLSE_TMA_PP32;
     static constexpr int NS = P + 4, NP = PP + 2, ND = (ORDER == ORDER_2SHOC) ? 4 : 0;
     static constexpr int DPX = TX + 2, DPY = TY + 2;
     static constexpr int up128(int b) { return (b + 127) / 128 * 128; }
@@ -1009,9 +1012,12 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
 #ifndef NLSE_F32_MINB
 #define NLSE_F32_MINB 1
 #endif
+#ifndef NLSE_F32_MINB8
+#define NLSE_F32_MINB8 3
+#endif
 template <typename T, int TYV>
 constexpr int t3_min_blocks() {
-    return TYV == 8 ? (sizeof(T) == 8 ? 2 : 3) : (sizeof(T) == 8 ? 1 : NLSE_F32_MINB);
+    return TYV == 8 ? (sizeof(T) == 8 ? 2 : NLSE_F32_MINB8) : (sizeof(T) == 8 ? 1 : NLSE_F32_MINB);
 }
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
 __global__ void __launch_bounds__(32 * TYV, t3_min_blocks<T, TYV>())
