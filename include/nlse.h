@@ -109,7 +109,8 @@ nlse_status nlse_get_psi_device(nlse_ctx *ctx, void *d_psi);
 nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
 
 /* ---------------------------------------------------------------- slab mode (§8(e))
- * A 3D grid partitioned into contiguous z slabs (a 2D grid into contiguous y-row slabs),
+ * A 3D grid partitioned into contiguous z slabs (a 2D grid into y-row slabs, a 1D grid into
+ * x segments),
  * one per rank (one GPU per process, or several "virtual ranks" in one process).  Rank r
  * owns global planes (rows) [z0, z0 + nloc) of nlse_slab_range over nz (ny).  Buffers read
  * with a halo carry w ghost planes (rows) on each side (w = 1 CD, 2 2SHOC); every stage
@@ -119,21 +120,20 @@ nlse_status nlse_step(nlse_ctx *ctx, double k, int64_t nsteps);
  *
  * In slab mode nlse_set_psi*, nlse_step and nlse_diagnostics are COLLECTIVE: every
  * rank calls them in the same order (like NCCL collectives).  Psi / V host buffers
- * hold the local slab (nloc planes / rows).  1D grids are not partitioned:
- * nlse_create_dist returns NLSE_ERR_ARG for ndim == 1 (a 1D job over several GPUs runs
- * one independent nlse_create context per GPU).  The 3D temporally blocked
- * CD path (two stages per pass) is single-GPU only; slab contexts use one pass per stage. */
+ * hold the local slab (nloc planes / rows / points).  The 3D temporally blocked CD path (two
+ * stages per pass), the 1D persistent CTA and the 2D cooperative stepper are single-GPU only;
+ * slab contexts use one pass per stage. */
 #define NLSE_MAX_RANKS 16
 #define NLSE_DIST_HANDLE_BYTES 512
 
-/* Balanced split of nz planes (or ny rows) over nranks: rank r gets nz/nranks, +1 for the
- * first nz % nranks ranks, starting at *z0.  Host only. */
+/* Balanced split of nz planes (ny rows in 2D, nx points in 1D) over nranks: rank r gets
+ * nz/nranks, +1 for the first nz % nranks ranks, starting at *z0.  Host only. */
 nlse_status nlse_slab_range(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *nloc);
 
-/* Create the slab context of `rank`: dims are the GLOBAL grid (ndim 2 or 3); V_local is
- * the rank's slab of V (nloc planes / rows) or NULL.  Errors as nlse_create, plus
- * NLSE_ERR_ARG if ndim == 1, a slab has fewer than 2w planes / rows, or rank/nranks are
- * out of range. */
+/* Create the slab context of `rank`: dims are the GLOBAL grid; the slab axis is the slowest
+ * one (z in 3D, y in 2D, x in 1D); V_local is the rank's slab of V or NULL.  Errors as
+ * nlse_create, plus NLSE_ERR_ARG if a slab has fewer than 2w planes / rows / points or
+ * rank/nranks are out of range. */
 nlse_status nlse_create_dist(int ndim, const int64_t dims[3], double h, double a, double s,
                              const double *V_local, nlse_bc bc, nlse_order order,
                              nlse_precision prec, uint32_t flags, int rank, int nranks,
@@ -223,7 +223,7 @@ typedef struct {
     int elem_bytes;            /* sizeof(real): 4 or 8 */
     char variant[64];          /* kernel family used for the interior */
     int rank, nranks;          /* slab mode (0, 1 otherwise) */
-    int64_t z0, nz_local;      /* owned global planes (2D: rows) [z0, z0 + nz_local) */
+    int64_t z0, nz_local;      /* owned global planes (2D: rows, 1D: points) [z0, z0 + nz_local) */
 } nlse_info;
 nlse_status nlse_get_info(nlse_ctx *ctx, nlse_info *out);
 

@@ -121,24 +121,30 @@ template <typename T> struct Consts {
 // The grid a context owns.  Single GPU: the whole grid.  Slab mode (§8(e)): the z
 // planes [z0, z0 + nz) of the global grid; the buffers read with a halo carry zghost
 // planes below plane 0 and above plane nz - 1, filled by the neighbours.
-// Slab mode partitions the slowest axis (the "slab axis": z in 3D, y in 2D): ns = its owned
-// length (nz in 3D, ny in 2D), su = the stride of one slab-axis step (sz in 3D, sy in 2D);
-// zf_lo / zf_hi / zghost refer to that axis.
+// Slab mode partitions the slowest axis (the "slab axis": z in 3D, y in 2D, x in 1D): ns = its
+// owned length (nz, ny, nx), su = the stride of one slab-axis step (sz, sy, 1); zf_lo / zf_hi /
+// zghost refer to that axis.
 struct Grid {
     int64_t nx, ny, nz;   // points per axis (unused = 1); 3D: nz = owned planes, 2D: ny = owned rows
     int64_t sy, sz;       // strides: sy = nx (or the pitched row), sz = sy*ny
     int64_t n;            // owned points
     int zf_lo, zf_hi;     // 1 if local slab-axis index 0 / ns - 1 is a global face (always 1 on one GPU)
     int zghost;           // ghost planes (3D) / rows (2D) on each side of the halo'd buffers (0 on one GPU)
-    int64_t ns, su;       // slab axis: owned length and stride (3D: nz, sz; 2D: ny, sy; 1D: 1, n)
+    int64_t ns, su;       // slab axis: owned length and stride (3D: nz, sz; 2D: ny, sy; 1D: nx, 1)
 };
 
-// 2D y-slab face tests (3D grids keep y = 0 / ny - 1 as faces): the low / high row of the owned
-// rows is a domain face only where the slab holds the global face (zf_lo / zf_hi)
+// 2D y-slab / 1D x-slab face tests (other axes keep 0 / n - 1 as faces): the low / high end of
+// the owned points along the slab axis is a domain face only where the slab holds the global
+// face (zf_lo / zf_hi)
 template <int DIM>
 __host__ __device__ __forceinline__ bool y_face(const Grid &g, int64_t j) {
     if (DIM == 2) return (g.zf_lo && j == 0) || (g.zf_hi && j == g.ny - 1);
     return j == 0 || j == g.ny - 1;
+}
+template <int DIM>
+__host__ __device__ __forceinline__ bool x_face(const Grid &g, int64_t i) {
+    if (DIM == 1) return (g.zf_lo && i == 0) || (g.zf_hi && i == g.nx - 1);
+    return i == 0 || i == g.nx - 1;
 }
 
 // global z-face test for a local plane index (DIM == 3)

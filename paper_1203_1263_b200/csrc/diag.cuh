@@ -45,7 +45,8 @@ diag_partial(const cplx<T> *__restrict__ Psi, const T *__restrict__ V, Grid g, d
         const double pr = p.x, pi = p.y;
         const double rho = pr * pr + pi * pi;
         double grad = 0.0;
-        if (i + 1 < g.nx) {
+        // x pairs (1D x-slabs: also across to the upper neighbour's first point, a ghost)
+        if (i + 1 < g.nx + ((DIM == 1 && !g.zf_hi) ? 1 : 0)) {
             const cplx<T> u = Psi[q + 1];
             const double dr = double(u.x) - pr, di = double(u.y) - pi;
             grad += dr * dr + di * di;

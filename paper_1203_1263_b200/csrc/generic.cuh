@@ -25,14 +25,15 @@ struct PointEval {
     __device__ __forceinline__ T v(int64_t q) const { return __ldg(V + q); }
 
     __device__ __forceinline__ int n_bnd(int64_t i, int64_t j, int64_t k) const {
-        int m = (i == 0 || i == g.nx - 1);
+        int m = x_face<DIM>(g, i);
         if (DIM >= 2) m += y_face<DIM>(g, j);
         if (DIM >= 3) m += is_zface(g, k);
         return m;
     }
     // Inward neighbour: one step in along every boundary axis (R-MSD-NBR).
     __device__ __forceinline__ void inward(int64_t &i, int64_t &j, int64_t &k) const {
-        i = (i == 0) ? 1 : (i == g.nx - 1 ? g.nx - 2 : i);
+        if (DIM == 1) i = (g.zf_lo && i == 0) ? 1 : ((g.zf_hi && i == g.nx - 1) ? g.nx - 2 : i);
+        else i = (i == 0) ? 1 : (i == g.nx - 1 ? g.nx - 2 : i);
         if (DIM == 3) j = (j == 0) ? 1 : (j == g.ny - 1 ? g.ny - 2 : j);
         if (DIM == 2) j = (g.zf_lo && j == 0) ? 1 : ((g.zf_hi && j == g.ny - 1) ? g.ny - 2 : j);
         if (DIM >= 3) k = (g.zf_lo && k == 0) ? 1 : ((g.zf_hi && k == g.nz - 1) ? g.nz - 2 : k);
@@ -168,7 +169,7 @@ struct PointEval {
 
 // The slab-axis index of (j, k): the plane in 3D, the row in 2D (neighbour stores, store_out).
 template <int DIM>
-__device__ __forceinline__ int64_t slab_index(int64_t j, int64_t k) { return DIM == 3 ? k : (DIM == 2 ? j : 0); }
+__device__ __forceinline__ int64_t slab_index(int64_t i, int64_t j, int64_t k) { return DIM == 3 ? k : (DIM == 2 ? j : i); }
 
 // One thread per grid point over the whole grid.
 template <typename T, int DIM, int ORDER, int BC, int STAGE>
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(256) stage_generic(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_any(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(i, j, k), F, psi);
 }
 
 // Boundary points only: a flat index over the boundary surface, mapped to (i,j,k).
@@ -200,9 +201,9 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
     // launch checks that the boundary count and a face fit in 31 bits
     const unsigned nx = unsigned(g.nx), ny = unsigned(g.ny);
     unsigned t = unsigned(t64);
-    if (DIM == 1) {
-        if (t >= 2u) return false;
-        i = t ? g.nx - 1 : 0; j = 0; k = 0;
+    if (DIM == 1) {                    // the x faces this slab holds
+        if (t >= unsigned(g.zf_lo + g.zf_hi)) return false;
+        i = (g.zf_lo && t == 0) ? 0 : g.nx - 1; j = 0; k = 0;
         return true;
     }
     const unsigned per = 2u * nx + (rows_only ? 0u : 2u * (ny - 2u));   // perimeter of one xy plane
@@ -244,7 +245,7 @@ __device__ __forceinline__ bool bnd_point(const Grid &g, int64_t t64, int64_t &i
 
 template <int DIM>
 __host__ __device__ inline int64_t n_boundary_points(const Grid &g, bool rows_only = false) {
-    if (DIM == 1) return 2;
+    if (DIM == 1) return g.zf_lo + g.zf_hi;
     if (DIM == 2) return (g.zf_lo + g.zf_hi) * g.nx + 2 * (g.ny - g.zf_lo - g.zf_hi);
     const int64_t per = 2 * g.nx + (rows_only ? 0 : 2 * (g.ny - 2));
     const int nf = g.zf_lo + g.zf_hi;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(256) stage_boundary(StageArgs<T> A) {
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_bnd(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(i, j, k), F, psi);
 }
 
 // 3D MSD boundary points with F(b') taken from what the interior kernel stored (A.fz /
@@ -303,18 +304,20 @@ template <typename T, int DIM, int ORDER, int BC, int STAGE>
 __global__ void __launch_bounds__(256) stage_interior_generic(StageArgs<T> A) {
     const int64_t k0 = DIM >= 3 ? A.g.zf_lo : 0;
     const int64_t j0 = DIM == 2 ? A.g.zf_lo : 1;                  // 2D: first owned interior row
-    const int64_t mx = A.g.nx - 2, my = DIM == 3 ? A.g.ny - 2 : (DIM == 2 ? A.g.ny - A.g.zf_lo - A.g.zf_hi : 1);
+    const int64_t i0 = DIM == 1 ? A.g.zf_lo : 1;                  // 1D: first owned interior point
+    const int64_t mx = DIM == 1 ? A.g.nx - A.g.zf_lo - A.g.zf_hi : A.g.nx - 2;
+    const int64_t my = DIM == 3 ? A.g.ny - 2 : (DIM == 2 ? A.g.ny - A.g.zf_lo - A.g.zf_hi : 1);
     const int64_t mz = DIM >= 3 ? A.g.nz - A.g.zf_lo - A.g.zf_hi : 1;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= mx * my * mz) return;
-    const int64_t i = 1 + t % mx;
+    const int64_t i = i0 + t % mx;
     const int64_t j = DIM >= 2 ? j0 + (t / mx) % my : 0;
     const int64_t k = DIM >= 3 ? k0 + t / (mx * my) : 0;
     PointEval<T, DIM, ORDER, BC> ev{A.Y, A.V, A.g, A.c};
     const int64_t q = ev.idx(i, j, k);
     cplx<T> F = ev.F_int(i, j, k);
     cplx<T> psi = (STAGE == 1) ? ev.y(q) : A.Psi[q];
-    rk_combine<STAGE, T>(A, q, slab_index<DIM>(j, k), F, psi);
+    rk_combine<STAGE, T>(A, q, slab_index<DIM>(i, j, k), F, psi);
 }
 
 }  // namespace nlse

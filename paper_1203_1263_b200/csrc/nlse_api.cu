@@ -244,7 +244,7 @@ void enqueue_add_steps(nlse_ctx *c, int64_t n) {
 }
 
 bool use_persist1d(const nlse_ctx *c) {
-    if (c->ndim != 1 || c->interior_kind == KK_GENERIC) return false;
+    if (c->ndim != 1 || c->interior_kind == KK_GENERIC || c->dist) return false;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
     const size_t need = c->prec == NLSE_FP64 ? persist1d_smem<double>(int(c->g.nx), c->hasV, c->order == NLSE_2SHOC4)
@@ -458,18 +458,18 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     if (dims[0] * dims[1] >= (int64_t(1) << 31) || dims[2] >= (int64_t(1) << 31))
         return fail(nullptr, NLSE_ERR_ARG, "an xy plane must have fewer than 2^31 points (32-bit in-plane indexing)");
     const int w = order == NLSE_2SHOC4 ? 2 : 1;
-    // slab axis (§8(e)): z in 3D, y in 2D; nloc = its owned length
-    const int sax = ndim == 3 ? 2 : 1;
+    // slab axis (§8(e)): z in 3D, y in 2D, x in 1D; nloc = its owned length
+    const int sax = ndim - 1;
     int64_t z0 = 0, nloc = dims[sax];
     if (dist) {
-        if (ndim < 2) return fail(nullptr, NLSE_ERR_ARG, "slab mode partitions 2D (y rows) and 3D (z planes) grids; 1D grids run as replicas");
         if (nranks < 1 || nranks > NLSE_MAX_RANKS || rank < 0 || rank >= nranks)
             return fail(nullptr, NLSE_ERR_ARG, "rank / nranks out of range");
         nlse_slab_range(dims[sax], nranks, rank, &z0, &nloc);
-        if (nloc < 2 * w) return fail(nullptr, NLSE_ERR_ARG, "every slab needs at least 2w planes / rows (w = 1 CD, 2 2SHOC)");
+        if (nloc < 2 * w) return fail(nullptr, NLSE_ERR_ARG, "every slab needs at least 2w planes / rows / points (w = 1 CD, 2 2SHOC)");
     }
+    const int64_t nx_own = ndim == 1 ? nloc : dims[0];
     const int64_t ny_own = ndim == 2 ? nloc : dims[1], nz_own = ndim == 3 ? nloc : 1;
-    const int64_t n = dims[0] * ny_own * nz_own;
+    const int64_t n = nx_own * ny_own * nz_own;
     if (V) {
         for (int64_t q = 0; q < n; q++)
             if (!std::isfinite(V[q])) return fail(nullptr, NLSE_ERR_ARG, "V must be finite");
@@ -483,8 +483,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     for (int d = 0; d < 3; d++) c->dims[d] = dims[d];
     c->h = h; c->a = a; c->s = s; c->bc = bc; c->order = order; c->prec = prec; c->flags = flags;
     c->dist = dist; c->rank = rank; c->nranks = nranks; c->z0 = z0;
-    c->g.nx = dims[0]; c->g.ny = ny_own; c->g.nz = nz_own;
-    c->g.sy = dims[0]; c->g.sz = dims[0] * ny_own; c->g.n = n;
+    c->g.nx = nx_own; c->g.ny = ny_own; c->g.nz = nz_own;
+    c->g.sy = nx_own; c->g.sz = nx_own * ny_own; c->g.n = n;
     c->eb = prec == NLSE_FP64 ? 8 : 4;
     // Pitched rows: the 3D TMA kernels need 16-byte row strides in every array (complex rows
     // 2*nx*eb, V rows nx*eb bytes); the paper pads rows the same way (cudaMallocPitch).
@@ -502,8 +502,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->g.zf_lo = (!dist || rank == 0) ? 1 : 0;
     c->g.zf_hi = (!dist || rank == nranks - 1) ? 1 : 0;
     c->g.zghost = dist ? w : 0;
-    c->g.ns = ndim == 3 ? c->g.nz : (ndim == 2 ? c->g.ny : 1);
-    c->g.su = ndim == 2 ? c->g.sy : c->g.sz;
+    c->g.ns = ndim == 3 ? c->g.nz : (ndim == 2 ? c->g.ny : c->g.nx);
+    c->g.su = ndim == 3 ? c->g.sz : (ndim == 2 ? c->g.sy : 1);
     c->hasV = V != nullptr;
     cudaGetDevice(&c->device);
     if (flags & NLSE_FLAG_GENERIC_KERNELS) c->interior_kind = KK_GENERIC;

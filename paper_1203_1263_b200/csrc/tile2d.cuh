@@ -310,11 +310,16 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
     const int64_t nx = A.g.nx;
     const int64_t x0 = int64_t(blockIdx.x) * T1_N;
     const int tid = threadIdx.x;
+    // x-slab mode (§8(e)): points [xmlo, xmhi) are in memory (ghosts of the neighbours); x faces
+    // only where the slab holds them; output points [olo, ohi]
+    const bool flo = A.g.zf_lo != 0, fhi = A.g.zf_hi != 0;
+    const int64_t xmlo = flo ? 0 : -A.g.zghost, xmhi = fhi ? nx : nx + A.g.zghost;
+    const int64_t olo = flo ? 1 : 0, ohi = fhi ? nx - 2 : nx - 1;
     // (1) Y tile with halo (zero outside the grid: never used)
     for (int e = tid; e < T1_N + 2 * H; e += T1_NT) {
         const int64_t gx = x0 - H + e;
         C v; v.x = T(0); v.y = T(0);
-        if (gx >= 0 && gx < nx) v = A.Y[gx];
+        if (gx >= xmlo && gx < xmhi) v = A.Y[gx];
         ys[e] = v;
     }
     __syncthreads();
@@ -330,9 +335,10 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
             const int lx = e - 1;
             const int64_t gx = x0 + lx;
             C d; d.x = T(NAN); d.y = T(NAN);
-            if (gx > 0 && gx < nx - 1) {
+            const bool face = (flo && gx == 0) || (fhi && gx == nx - 1);
+            if (!face && gx > xmlo && gx < xmhi - 1) {
                 d = d_int(lx);
-            } else if (gx == 0 || gx == nx - 1) {
+            } else if (face) {
                 if (BC == BC_L0) {
                     d.x = T(0); d.y = T(0);
                 } else {
@@ -365,7 +371,7 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
     for (int r = 0; r < T1_R; r++) {
         const int lx = tid + r * T1_NT;
         const int64_t q = x0 + lx;
-        if (q < 1 || q > nx - 2) continue;
+        if (q < olo || q > ohi) continue;
         const C yc = Yl(lx);
         C L;
         if (ORDER == ORDER_CD) L = d_int(lx);
@@ -375,11 +381,11 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
         C F = f_lin(A.c.a, L, sr, yc);
         if (A.V) F = f_addv(F, __ldg(A.V + q), yc);
         const C psi = STAGE == 1 ? yc : A.Psi[q];
-        rk_combine<STAGE, T>(A, q, 0, F, psi);
-        // the boundary point whose b' is q (nx = 3: q = 1 is b' of both)
+        rk_combine<STAGE, T>(A, q, q, F, psi);
+        // the boundary point whose b' is q (nx = 3: q = 1 is b' of both); held faces only
         for (int side = 0; side < 2; side++) {
             const int64_t qb = side == 0 ? 0 : nx - 1;
-            if (q != (side == 0 ? 1 : nx - 2)) continue;
+            if (!(side == 0 ? flo : fhi) || q != (side == 0 ? 1 : nx - 2)) continue;
             const C yb = Yl(int(qb - x0));
             C Fb;
             if (BC == BC_DIRICHLET) {
@@ -402,7 +408,7 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
                 Fb.y = m * yb.x;
             }
             const C psib = STAGE == 1 ? yb : A.Psi[qb];
-            rk_combine<STAGE, T>(A, qb, 0, Fb, psib);
+            rk_combine<STAGE, T>(A, qb, qb, Fb, psib);
         }
     }
 }

@@ -139,14 +139,14 @@ class Solver:
     """Owns one nlse_ctx.  dims = (nx,), (nx, ny) or (nx, ny, nz) (the GLOBAL grid); numpy arrays
     have shape reversed(dims) (x fastest).  dist=(rank, nranks) creates a slab-mode context
     (nlse_create_dist): Psi / V arrays then hold the local slab, shape (nloc, ny, nx) in 3D
-    (z planes) or (nloc, nx) in 2D (y rows)."""
+    (z planes), (nloc, nx) in 2D (y rows) or (nloc,) in 1D (x points)."""
 
     def __init__(self, dims, h, a=1.0, s=1.0, V=None, bc="dirichlet", scheme="2shoc", precision="fp64",
                  force_dt=False, generic=False, dist=None):
         self.dims = tuple(int(d) for d in dims)
         self.dist = dist
-        if dist is not None and len(self.dims) >= 2:
-            # slab axis: z (3D) or y (2D), the slowest axis of the (.., y, x) arrays
+        if dist is not None:
+            # slab axis: z (3D), y (2D) or x (1D), the slowest axis of the (.., y, x) arrays
             rank, nranks = dist
             self.z0, nloc = nlse_slab_range(self.dims[-1], nranks, rank)
             self.shape = (nloc,) + tuple(reversed(self.dims[:-1]))

@@ -94,7 +94,7 @@ def test_slab_errors():
         Solver((20, 20, 7), 0.5, scheme="2shoc", dist=(1, 2))       # 4 + 3 planes: 3 < 2w
     assert e.value.status == NLSE_ERR_ARG
     with pytest.raises(NLSEError) as e:
-        Solver((200,), 0.5, dist=(0, 2))                            # 1D is not partitioned
+        Solver((7,), 0.5, scheme="2shoc", dist=(1, 2))              # 1D: 4 + 3 points: 3 < 2w
     assert e.value.status == NLSE_ERR_ARG
     with pytest.raises(NLSEError) as e:
         Solver((20, 7), 0.5, scheme="2shoc", dist=(1, 2))           # 2D: 4 + 3 rows: 3 < 2w
@@ -157,5 +157,42 @@ def test_2d_slabs_match_oracle_chunks_thin_and_diagnostics(generic):
         ref = run_oracle(dims, h, psi0, k, 10, s=-1.0, V=V, bc="msd", scheme=scheme)
         out, (m, e) = run_gpu_slabs(dims, h, psi0, k, 10, P, chunks=[3, 1, 6], diag=True, **kw)
         assert ulp_diff(out, ref, "fp64") == 0, (dims, P)
+        mo, eo = oracle.diagnostics(oracle.Problem(dims, h, a=1.0, s=-1.0, bc="msd"), out, V)
+        assert len(set(m)) == 1 and abs(m[0] - mo) <= 1e-12 * abs(mo) and abs(e[0] - eo) <= 1e-12 * abs(eo)
+
+
+# ---------------------------------------------------------------------------------------------
+# 1D x slabs (§8(f) rank 4, "large-1D split"): the slab axis is x; w ghost points on each side
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+@pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("generic", [False, True], ids=["tile", "generic"])
+def test_1d_slabs_bitwise_equal_single(scheme, bc, precision, withV, nranks, generic):
+    dims, h = (4099,), 0.05          # slabs cut the 1024-point tiles anywhere
+    psi0 = case_input(dims, seed=55)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=56)) if withV else None
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision, generic=generic)
+    k = 0.5 * h * h / math.sqrt(2) * (0.75 if scheme == "2shoc" else 1.0)
+    one = run_gpu(dims, h, psi0, k, 9, **kw)
+    many = run_gpu_slabs(dims, h, psi0, k, 9, nranks, **kw)
+    assert ulp_diff(many, one, precision) == 0
+
+
+def test_1d_slabs_oracle_thin_and_diagnostics():
+    import oracle
+    h = 0.1
+    for n, P, scheme in [(1001, 4, "2shoc"), (8, 2, "2shoc"), (13, 3, "2shoc"), (6, 3, "cd")]:
+        dims = (n,)
+        psi0 = case_input(dims, seed=57)
+        V = np.abs(inputs.random_smooth(dims, seed=58))
+        k = 0.5 * h * h / math.sqrt(2) * (0.75 if scheme == "2shoc" else 1.0)
+        ref = run_oracle(dims, h, psi0, k, 10, s=-1.0, V=V, bc="msd", scheme=scheme)
+        out, (m, e) = run_gpu_slabs(dims, h, psi0, k, 10, P, s=-1.0, V=V, bc="msd", scheme=scheme, chunks=[3, 7],
+                                    diag=True)
+        assert ulp_diff(out, ref, "fp64") == 0, (n, P)
         mo, eo = oracle.diagnostics(oracle.Problem(dims, h, a=1.0, s=-1.0, bc="msd"), out, V)
         assert len(set(m)) == 1 and abs(m[0] - mo) <= 1e-12 * abs(mo) and abs(e[0] - eo) <= 1e-12 * abs(eo)
