@@ -23,7 +23,8 @@ thread_local std::string nlse_rt::g_create_error;
 namespace {
 
 const char *kKindName[KK_COUNT] = {"stage_generic", "stage3d_stream", "stage3d_tma", "stage2d_tile",
-                                   "stage1d_tile", "stage_boundary", "diag", "peer_barrier", "fused3d_cd"};
+                                   "stage1d_tile", "stage_boundary", "diag", "peer_barrier", "fused3d_cd",
+                                   "stage2d_strip"};
 
 struct DistBlob {               // what nlse_dist_export writes (NLSE_DIST_HANDLE_BYTES)
     uint32_t magic, version;
@@ -507,7 +508,16 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
     c->hasV = V != nullptr;
     cudaGetDevice(&c->device);
     if (flags & NLSE_FLAG_GENERIC_KERNELS) c->interior_kind = KK_GENERIC;
-    else c->interior_kind = ndim == 3 ? KK_TMA3D : (ndim == 2 ? KK_TILE2D : KK_TILE1D);
+    else c->interior_kind = ndim == 3 ? KK_TMA3D : (ndim == 2 ? KK_STRIP2D : KK_TILE1D);
+    // 2D: the warp-strip kernel (strip2d.cuh, boundary included, one launch per stage) by default;
+    // NLSE_2D_KERNEL=tile selects the round-1 shared-tile kernel + boundary kernel
+    if (c->interior_kind == KK_STRIP2D) {
+        const char *e2 = getenv("NLSE_2D_KERNEL");
+        const char *ep2 = getenv("NLSE_PERSIST2D");    // (the persistent stepper runs the tile body)
+        // (the strip kernel addresses rows by 32-bit element offsets)
+        const bool fits = (c->g.ny + 2 * int64_t(c->g.zghost) + 1) * c->g.sy < (int64_t(1) << 31);
+        if ((e2 && std::string(e2) == "tile") || (ep2 && ep2[0] == '1') || !fits) c->interior_kind = KK_TILE2D;
+    }
 
     auto bail = [&](nlse_status st) { g_create_error = c->err; nlse_destroy(c); return st; };
 #define CREATE_TRY(expr)                                                                         \
@@ -1076,7 +1086,7 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     if (!out) return fail(c, NLSE_ERR_ARG, "out is NULL");
     memset(out, 0, sizeof *out);
     out->points = c->g.n;
-    int per_stage = (c->interior_kind == KK_GENERIC || c->interior_kind == KK_TILE1D) ? 1 : 2;
+    int per_stage = (c->interior_kind == KK_GENERIC || c->interior_kind == KK_TILE1D || c->interior_kind == KK_STRIP2D) ? 1 : 2;
     if (c->dist && c->nranks > 1) per_stage += 1;
     out->launches_per_step = (c->persist1d || c->persist2d) ? 0 : (c->fused ? 4 : 4 * per_stage);   // 0: one launch per nlse_step call
     const int64_t cbytes = 2 * c->eb, rv = c->hasV ? c->eb : 0;

@@ -21,7 +21,7 @@
 #include "common.cuh"
 
 enum KernelKind { KK_GENERIC = 0, KK_STREAM3D, KK_TMA3D, KK_TILE2D, KK_TILE1D, KK_BOUNDARY, KK_DIAG, KK_COMM,
-                  KK_FUSED3D, KK_COUNT };
+                  KK_FUSED3D, KK_STRIP2D, KK_COUNT };
 static_assert(KK_COUNT <= NLSE_MAX_KINDS, "too many kernel kinds");
 
 struct TimedLaunch { int kind; cudaEvent_t a, b; int64_t points; };

@@ -11,6 +11,7 @@
 #include "stream3d.cuh"
 #include "tile2d.cuh"
 #include "fused3d.cuh"
+#include "strip2d.cuh"
 
 namespace nlse_rt {
 
@@ -92,6 +93,13 @@ void launch_stage(nlse_ctx *c, const StageArgs<T> &A) {
         LaunchTimer lt(c, KK_GENERIC, c->g.n);
         stage_generic<T, DIM, ORDER, BC, STAGE><<<blocks_for(c->g.n, 256), 256, 0, c->stream>>>(A);
         return;
+    }
+    if constexpr (DIM == 2) {
+        if (c->interior_kind == KK_STRIP2D) {          // boundary included: one launch per stage
+            LaunchTimer lt(c, KK_STRIP2D, c->g.n);
+            launch_strip2d<T, ORDER, BC, STAGE>(A, c->nsm, c->stream);
+            return;
+        }
     }
     // 2D/3D: the boundary kernel (disjoint outputs, same inputs: it recomputes what it needs at
     // b') runs concurrently on a side stream, forked from and joined back into the context

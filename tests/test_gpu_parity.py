@@ -23,16 +23,21 @@ def _k(ndim, h, scheme):
 
 
 @pytest.mark.parametrize("kernel", ["fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on", "v1",
-                                    "generic"])
+                                    "tile2d", "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 @pytest.mark.parametrize("ndim", [1, 2, 3])
 def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch):
-    """Every kernel family against the oracle: "fast" = the default (3D: TMA z-streaming),
-    "v1" = the cp.async z-streaming kernel (3D), "generic" = one thread per point."""
-    if kernel != "fast" and kernel != "generic" and ndim != 3:
+    """Every kernel family against the oracle: "fast" = the default (3D: TMA z-streaming, 2D: warp
+    strips), "v1" = the cp.async z-streaming kernel (3D), "tile2d" = the shared-tile 2D kernel +
+    boundary kernel, "generic" = one thread per point."""
+    if kernel == "tile2d":
+        if ndim != 2:
+            pytest.skip("tile2d is a 2D kernel variant")
+        monkeypatch.setenv("NLSE_2D_KERNEL", "tile")
+    elif kernel != "fast" and kernel != "generic" and ndim != 3:
         pytest.skip(f"{kernel} is a 3D kernel variant")
     if kernel == "v1":
         monkeypatch.setenv("NLSE_3D_KERNEL", "v1")
@@ -56,11 +61,12 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
-    want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_tile", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+    want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_strip", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+            "tile2d": "stage2d_tile",
             "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma", "msd_recompute": "stage3d_tma", "xfuse_off": "stage3d_tma", "xfuse_on": "stage3d_tma",
             "generic": "stage_generic"}[kernel]
     if not (kernel in ("fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
-        assert info["variant"] == want or (want, info["variant"]) == ("stage2d_tile", "rk4_2d_persistent"), info
+        assert info["variant"] == want, info
     assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV} {info['variant']}")
 
 

@@ -127,7 +127,7 @@ def test_full_step_counts_match_oracle_digest(name):
 def test_2d_persistent_and_per_stage_bitwise(scheme, bc, precision, persist, monkeypatch):
     """2D grids up to 2^21 points run every stage of an nlse_step call in one cooperative launch
     (rk4_2d_persistent: grid-wide barriers between stages); NLSE_PERSIST2D=0 forces the per-stage
-    kernels.  Both bit for bit against the oracle, chunked calls included."""
+    kernels (the default warp-strip kernel).  Both bit for bit against the oracle, chunked calls included."""
     monkeypatch.setenv("NLSE_PERSIST2D", persist)
     dims, h = (133, 70), 0.2
     psi0 = case_input(dims, seed=61)
@@ -136,7 +136,7 @@ def test_2d_persistent_and_per_stage_bitwise(scheme, bc, precision, persist, mon
     k = _k(2, h, scheme)
     ref = run_oracle(dims, h, psi0, k, 19, **kw)
     got, info = run_gpu(dims, h, psi0, k, 19, chunks=[1, 17, 1], with_info=True, **kw)
-    assert info["variant"] == ("rk4_2d_persistent" if persist == "1" else "stage2d_tile"), info
+    assert info["variant"] == ("rk4_2d_persistent" if persist == "1" else "stage2d_strip"), info
     assert_parity(got, ref, precision, what=f"2D persist={persist} {scheme} {bc} {precision}")
 
 

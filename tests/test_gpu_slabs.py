@@ -131,7 +131,10 @@ def test_virtual_group_requires_group_calls():
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
-def test_2d_slabs_bitwise_equal_single(scheme, bc, precision, withV, nranks):
+@pytest.mark.parametrize("kernel", ["strip", "tile"])
+def test_2d_slabs_bitwise_equal_single(scheme, bc, precision, withV, nranks, kernel, monkeypatch):
+    if kernel == "tile":
+        monkeypatch.setenv("NLSE_2D_KERNEL", "tile")
     dims = (133, 70)             # tiles of 32 x 16 with ragged tails; slabs cut tiles anywhere
     h = 0.2
     psi0 = case_input(dims, seed=51)
@@ -143,11 +146,17 @@ def test_2d_slabs_bitwise_equal_single(scheme, bc, precision, withV, nranks):
     assert ulp_diff(many, one, precision) == 0
 
 
-@pytest.mark.parametrize("generic", [False, True])
-def test_2d_slabs_match_oracle_chunks_thin_and_diagnostics(generic):
+@pytest.mark.parametrize("kernel", ["strip", "strip_rows3", "tile", "generic"])
+def test_2d_slabs_match_oracle_chunks_thin_and_diagnostics(kernel, monkeypatch):
     """2D slabs against the oracle (chunked calls, CUDA graphs not used by virtual groups),
-    slabs of exactly 2w rows and uneven splits, the generic kernels, global diagnostics."""
+    slabs of exactly 2w rows and uneven splits, the warp-strip kernel (also with 3-row chunks),
+    the shared-tile kernel, the generic kernels, global diagnostics."""
     import oracle
+    generic = kernel == "generic"
+    if kernel == "tile":
+        monkeypatch.setenv("NLSE_2D_KERNEL", "tile")
+    if kernel == "strip_rows3":
+        monkeypatch.setenv("NLSE_STRIP_ROWS", "3")
     h = 0.25
     for dims, P, scheme in [((64, 48), 3, "2shoc"), ((40, 8), 2, "2shoc"), ((40, 13), 3, "2shoc"), ((37, 6), 3, "cd")]:
         psi0 = case_input(dims, seed=53)
