@@ -63,10 +63,8 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
         if (best < 0 || cost < best) { best = cost; zchunk = ch; }
         if (ch <= 4) break;
     }
-    static const int64_t env_chunk = [] {
-        const char *e = getenv("NLSE_ZCHUNK");
-        return e ? std::atoll(e) : int64_t(0);
-    }();
+    const char *ezc = getenv("NLSE_ZCHUNK");               // (read per launch: tests vary it)
+    const int64_t env_chunk = ezc ? std::atoll(ezc) : int64_t(0);
     if (env_chunk > 0) zchunk = env_chunk;
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
