@@ -22,8 +22,8 @@ def _k(ndim, h, scheme):
     return 0.5 * kb
 
 
-@pytest.mark.parametrize("kernel", ["fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on", "v1",
-                                    "tile2d", "generic"])
+@pytest.mark.parametrize("kernel", ["fast", "edge_off", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on",
+                                    "v1", "tile2d", "generic"])
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
@@ -49,8 +49,9 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
         if bc != "msd":
             pytest.skip("MSD only")
         monkeypatch.setenv("NLSE_XFUSE", "0" if kernel == "xfuse_off" else "1")
-    if kernel.startswith("edge"):       # every TMA tile on the lean face-aware loop / per-point face path
-        monkeypatch.setenv("NLSE_FORCE_EDGE", "1" if kernel == "edge_lean" else "2")
+    if kernel.startswith("edge"):       # interior tiles on the branch-free loop (0) / every TMA tile on the lean
+        # face-aware loop (1) / on the per-point face path (2); default: 1 where most tiles touch a face
+        monkeypatch.setenv("NLSE_FORCE_EDGE", {"edge_off": "0", "edge_lean": "1", "edge_pp": "2"}[kernel])
     generic = kernel == "generic"
     dims = DIMS[ndim]
     h = H[ndim]
@@ -62,18 +63,19 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
     want = {"fast": {1: "rk4_1d_persistent", 2: "stage2d_strip", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
-            "tile2d": "stage2d_tile",
+            "tile2d": "stage2d_tile", "edge_off": "stage3d_tma",
             "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma", "msd_recompute": "stage3d_tma", "xfuse_off": "stage3d_tma", "xfuse_on": "stage3d_tma",
             "generic": "stage_generic"}[kernel]
-    if not (kernel in ("fast", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
+    if not (kernel in ("fast", "edge_off", "edge_lean", "edge_pp", "msd_recompute", "xfuse_off", "xfuse_on") and ndim == 3 and precision == "fp32" and withV):   # fp32 V rows: 4*70 B
         assert info["variant"] == want, info
     assert_parity(got, ref, precision, what=f"{ndim}D {scheme} {bc} {precision} V={withV} {info['variant']}")
 
 
+@pytest.mark.parametrize("force_edge", ["auto", "0"])
 @pytest.mark.parametrize("dims", [(65, 33, 9), (33, 17, 7), (64, 31, 8), (97, 49, 6), (63, 47, 7), (35, 20, 6)])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-def test_tile_alignment_cases(dims, bc, precision):
+def test_tile_alignment_cases(dims, bc, precision, force_edge, monkeypatch):
     """3D grids whose faces fall on every tile position the TMA kernel distinguishes: a face one
     past a tile (nx = 32k + 1, ny = 16k + 1: the face is on the neighbour tile's ring), a face on
     lane 0 of a tile (x-face b' on the previous tile), faces on the last lane / row, ragged."""
