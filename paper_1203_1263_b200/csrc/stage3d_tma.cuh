@@ -1023,13 +1023,27 @@ template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
 __global__ void __launch_bounds__(32 * TYV, t3_min_blocks<T, TYV>())
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
-            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge) {
+            const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge, int band) {
     using Cfg = T3Cfg<T, ORDER, P, TYV, STAGE != 1>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int ntiles = ntx * nty;
     const int w = blockIdx.x;
     const int c = w / ntiles, t = w - c * ntiles;
-    const int x0 = (t % ntx) * Cfg::TX, y0 = (t / ntx) * Cfg::TY;
+    // tile order within a z chunk: row-major (band = 0), or bands of `band` tile rows walked column
+    // by column, so that the tiles sharing a y halo start within a few CTAs of each other (their
+    // halo planes are then L2 hits; row-major puts a tile's y neighbour a whole tile row, ~30 planes
+    // of progress, ahead)
+    int tx_, ty_;
+    if (band > 1) {
+        const int b = t / (band * ntx), u = t - b * band * ntx;
+        const int rows = min(band, nty - b * band);
+        tx_ = u / rows;
+        ty_ = b * band + (u - tx_ * rows);
+    } else {
+        tx_ = t % ntx;
+        ty_ = t / ntx;
+    }
+    const int x0 = tx_ * Cfg::TX, y0 = ty_ * Cfg::TY;
     const int nz = int(A.g.nz);
     const int zlo = A.g.zf_lo ? 1 : 0, zhi = nz - (A.g.zf_hi ? 1 : 0);
     const int zs = zlo + c * zchunk;

@@ -69,6 +69,11 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
     if (zchunk > mz) zchunk = mz;
     const unsigned gz = unsigned((mz + zchunk - 1) / zchunk);
     const int64_t items = int64_t(gx) * gy * gz;
+    // tile order (stage3d_tma): bands of 4 tile rows walked column by column where there are at
+    // least 8 tile rows (1024^3: 78.8 vs 80.6 DRAM bytes per point-stage, -0.6 % step time, r02
+    // band); NLSE_TILE_BAND=0 row-major, =B bands of B rows
+    const char *eband = getenv("NLSE_TILE_BAND");
+    const int band = eband ? std::atoi(eband) : (gy >= 8 ? 4 : 0);
     // debug / measurement / tests: NLSE_FORCE_EDGE=1 runs every tile on the face-aware lean
     // loop, =2 every tile on the per-point face path (t3_run, EDGE)
     const char *fe = getenv("NLSE_FORCE_EDGE");
@@ -86,7 +91,7 @@ void launch_tma3d_ty(nlse_ctx *c, const StageArgs<T> &A) {
         force_edge = (2 * inner(nx, Cfg::TX) * inner(ny, Cfg::TY) < cols) ? 1 : 0;
     }
     kern<<<unsigned(items), Cfg::NT, Cfg::SMEM, c->stream>>>(c->maps.y[ybuf_of_stage(STAGE)], c->maps.psi, c->maps.k,
-                                                          c->maps.v, A, int(zchunk), int(gx), int(gy), force_edge);
+                                                          c->maps.v, A, int(zchunk), int(gx), int(gy), force_edge, band);
 }
 
 template <typename T, int ORDER, int BC, int STAGE>

@@ -89,6 +89,22 @@ def test_tile_alignment_cases(dims, bc, precision, force_edge, monkeypatch):
     assert_parity(got, ref, precision, what=f"{dims} {bc} {precision}")
 
 
+@pytest.mark.parametrize("band", ["0", "1", "3", "4", "16"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_tile_band_orders(band, precision, monkeypatch):
+    """The 3D TMA kernel's tile order within a z chunk (row-major, or bands of B tile rows walked
+    column by column, the last band partial): every tile exactly once, bit for bit."""
+    monkeypatch.setenv("NLSE_TILE_BAND", band)
+    dims = (70, 146, 6)              # 3 x 10 tiles of 32 x 16 (fp64) / 3 x 19 of 32 x 8 (fp32)
+    psi0 = case_input(dims, seed=44)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=45))
+    h = 0.5
+    kw = dict(a=0.9, s=-1.1, V=V, bc="msd", scheme="2shoc", precision=precision)
+    ref = run_oracle(dims, h, psi0, _k(3, h, "2shoc"), 4, **kw)
+    got = run_gpu(dims, h, psi0, _k(3, h, "2shoc"), 4, **kw)
+    assert_parity(got, ref, precision, what=f"band {band} {precision}")
+
+
 @pytest.mark.parametrize("dims", [(3,), (4,), (3, 3), (3, 5), (5, 3), (3, 3, 3), (4, 3, 5), (3, 7, 3), (9, 3, 4)])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
