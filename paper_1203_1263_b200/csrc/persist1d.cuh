@@ -1,17 +1,15 @@
 // persist1d.cuh -- 1D grids: all RK4 steps of one nlse_step call in ONE CTA, with the
-// whole state (Psi, K_tot, Psi_tmp, Psi_out, D, F and V) resident in shared memory.
+// whole state (Psi, K_tot, Psi_tmp, Psi_out and V) resident in shared memory.
 //
 // The 1D configurations (1025-2001 points) are latency-bound:
 // per stage there are only ~2000 points of work, so eight kernel launches per step would
-// cost far more than the arithmetic.  Here a stage is three block-wide phases separated
-// by __syncthreads:
-//   (1) 2SHOC step 1, D = Delta_2 Y / h^2 ((2shoc1d) P:197) at every point, boundary
-//       points by the Laplacian form of the BC ((BCDlap) P:320-323, (BCMSDlap) P:336-344,
-//       (BCL0lap) P:352-355);
-//   (2) interior points: L ((2shoc1d2) P:198, or L = D for CD), F (fsplit) P:424-428, F
-//       kept in shared memory, and the RK4 stage combine (RK4_GPU) P:495-519;
-//   (3) the two boundary points: F from the time-derivative BC ((BCDdt) P:315-318,
-//       (msd) P:331-335 with F at b' from phase 2, (BCL0dt) P:347-350) and the combine.
+// cost far more than the arithmetic.  Here a stage is ONE block-wide phase (round 2; it was
+// three, separated by barriers): every thread evaluates, for each of its points, 2SHOC step 1
+// D = Delta_2 Y / h^2 ((2shoc1d) P:197) at the point and its two neighbours itself (boundary
+// points by the Laplacian form of the BC, (BCDlap) P:320-323, (BCMSDlap) P:336-344, (BCL0lap)
+// P:352-355), step 2 ((2shoc1d2) P:198; CD: L = D), F (fsplit) P:424-428 and the RK4 stage
+// combine (RK4_GPU) P:495-519; the two boundary points recompute F at b' themselves ((BCDdt)
+// P:315-318, (msd) P:331-335, (BCL0dt) P:347-350).  One __syncthreads per stage.
 // Every value follows the DAG of DESIGN.md §3.1 (the same expressions as generic.cuh),
 // so the result is bit-identical to the oracle and to the per-stage kernels.
 #pragma once
@@ -20,6 +18,9 @@
 namespace nlse {
 
 constexpr int P1_THREADS = 1024;
+#ifndef NLSE_P1_MSD2
+#define NLSE_P1_MSD2 1
+#endif
 
 template <typename T>
 struct Persist1DArgs {
@@ -34,7 +35,9 @@ struct Persist1DArgs {
 
 template <typename T>
 inline size_t persist1d_smem(int n, bool hasV, bool shoc) {
-    return size_t(n) * (sizeof(cplx<T>) * (5 + (shoc ? 1 : 0)) + (hasV ? sizeof(T) : 0));
+    (void)shoc;                          // (round 2: no D / F arrays, one phase per stage)
+    // Psi, K_tot, Psi_tmp, Psi_out, F at points 1 and n - 2 (MSD), V
+    return size_t(n) * sizeof(cplx<T>) * 4 + 2 * sizeof(cplx<T>) + (hasV ? size_t(n) * sizeof(T) : 0);
 }
 
 template <typename T, int ORDER, int BC>
@@ -43,9 +46,9 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = P.n;
     C *Ps = reinterpret_cast<C *>(smem_raw);
-    C *Ks = Ps + n, *As = Ks + n, *Bs = As + n, *Fs = Bs + n;
-    C *Ds = Fs + n;                                            // 2SHOC only
-    T *Vs = reinterpret_cast<T *>(Ds + (ORDER == ORDER_2SHOC ? n : 0));
+    C *Ks = Ps + n, *As = Ks + n, *Bs = As + n;
+    C *Fb = Bs + n;                                            // MSD: F at points 1, n - 2
+    T *Vs = reinterpret_cast<T *>(Fb + 2);
     const bool hasV = P.V != nullptr;
     for (int i = threadIdx.x; i < n; i += P1_THREADS) {
         Ps[i] = P.psi[i];
@@ -92,57 +95,67 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
                     Out[i] = cfma(c.kc, F, Ps[i]);
                 }
             };
-            // (1) 2SHOC step 1 with boundary D from the Laplacian form of the BC
-            if (ORDER == ORDER_2SHOC) {
-                for (int i = threadIdx.x; i < n; i += P1_THREADS) {
-                    C d;
-                    if (i > 0 && i < n - 1) {
-                        d = d_int(c, Y, i);
-                    } else if (BC == BC_L0) {
-                        d.x = T(0); d.y = T(0);
-                    } else {
-                        const C yb = Y[i];
-                        const T nb = nlin(c, i, yb);
-                        if (BC == BC_DIRICHLET) {
-                            const T t = c.inv_a * nb;
-                            d.x = -(t * yb.x); d.y = -(t * yb.y);
-                        } else {
-                            const int i1 = i == 0 ? 1 : n - 2;
-                            const C y1 = Y[i1], d1 = d_int(c, Y, i1);
-                            const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
-                            T re = T(0);
-                            if (!(rho1 < c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
-                            const T n1 = nlin(c, i1, y1);
-                            const T g = re + ((n1 - nb) * c.inv_a);
-                            d = cscale(g, yb);
-                        }
-                    }
-                    Ds[i] = d;
+            // D at point j: 2SHOC step 1 at interior points, the Laplacian form of the BC at the two
+            // boundary points (with D_int and Y at b')
+            auto d_any = [&](int j) -> C {
+                if (j > 0 && j < n - 1) return d_int(c, Y, j);
+                C d;
+                if (BC == BC_L0) {
+                    d.x = T(0); d.y = T(0);
+                    return d;
                 }
-                __syncthreads();
-            }
-            // (2) interior: L, F, combine
-            for (int i = 1 + threadIdx.x; i < n - 1; i += P1_THREADS) {
-                C L;
-                if (ORDER == ORDER_CD) L = d_int(c, Y, i);
-                else L = cfma(c.c76, Ds[i], cneg(cscale(c.c112, cadd(Ds[i - 1], Ds[i + 1]))));
-                const C F = f_of(c, i, Y[i], L);
-                Fs[i] = F;
-                combine(i, F);
-            }
-            __syncthreads();
-            // (3) boundary points
-            if (threadIdx.x < 2) {
-                const int i = threadIdx.x == 0 ? 0 : n - 1;
-                C F;
+                const C yb = Y[j];
+                const T nb = nlin(c, j, yb);
                 if (BC == BC_DIRICHLET) {
+                    const T t = c.inv_a * nb;
+                    d.x = -(t * yb.x); d.y = -(t * yb.y);
+                } else {
+                    const int j1 = j == 0 ? 1 : n - 2;
+                    const C y1 = Y[j1], d1 = d_int(c, Y, j1);
+                    const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+                    T re = T(0);
+                    if (!(rho1 < c.eps2)) re = ((d1.x * y1.x) + (d1.y * y1.y)) / rho1;
+                    const T n1 = nlin(c, j1, y1);
+                    const T g = re + ((n1 - nb) * c.inv_a);
+                    d = cscale(g, yb);
+                }
+                return d;
+            };
+            // F at interior point j: L ((2shoc1d2) P:198 from D at j-1, j, j+1, each evaluated here;
+            // CD: L = D), (fsplit) P:424-428
+            auto f_int = [&](int j) -> C {
+                C L;
+                if (ORDER == ORDER_CD) L = d_int(c, Y, j);
+                else L = cfma(c.c76, d_any(j), cneg(cscale(c.c112, cadd(d_any(j - 1), d_any(j + 1)))));
+                return f_of(c, j, Y[j], L);
+            };
+            // One phase per stage: every point of this thread, the boundary points with F(b')
+            // recomputed locally ((BCDdt) P:315-318, (msd) P:331-335, (BCL0dt) P:347-350), so the
+            // only barrier is the one before the next stage reads this stage's output.  (D is
+            // evaluated up to three times per point instead of once through shared memory: the
+            // same expressions, so the same bits, and two block barriers fewer per stage.)
+            // MSD (NLSE_P1_MSD2, default): the two boundary points take F(b') from the threads of
+            // points 1 and n - 2 through shared memory after a second barrier, instead of
+            // recomputing it (two dependent divisions on one thread's critical path)
+            constexpr bool MSD2 = BC == BC_MSD && NLSE_P1_MSD2;
+            for (int i = threadIdx.x; i < n; i += P1_THREADS) {
+                C F;
+                if (i > 0 && i < n - 1) {
+                    F = f_int(i);
+                    if (MSD2) {
+                        if (i == 1) Fb[0] = F;
+                        if (i == n - 2) Fb[1] = F;
+                    }
+                } else if (MSD2) {
+                    continue;
+                } else if (BC == BC_DIRICHLET) {
                     F.x = T(0); F.y = T(0);
                 } else if (BC == BC_L0) {
                     C z; z.x = T(0); z.y = T(0);
                     F = f_of(c, i, Y[i], z);
                 } else {
                     const int i1 = i == 0 ? 1 : n - 2;
-                    const C y1 = Y[i1], f1 = Fs[i1], yb = Y[i];
+                    const C y1 = Y[i1], f1 = f_int(i1), yb = Y[i];
                     const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
                     T m = T(0);
                     if (!(rho1 < c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
@@ -150,6 +163,20 @@ __global__ void __launch_bounds__(P1_THREADS, 1) rk4_1d_persistent(Persist1DArgs
                     F.y = m * yb.x;
                 }
                 combine(i, F);
+            }
+            if (MSD2) {
+                __syncthreads();
+                if (threadIdx.x < 2) {
+                    const int i = threadIdx.x == 0 ? 0 : n - 1, i1 = i == 0 ? 1 : n - 2;
+                    const C y1 = Y[i1], f1 = Fb[threadIdx.x], yb = Y[i];
+                    const T rho1 = (y1.x * y1.x) + (y1.y * y1.y);
+                    T m = T(0);
+                    if (!(rho1 < c.eps2)) m = ((f1.y * y1.x) - (f1.x * y1.y)) / rho1;
+                    C F;
+                    F.x = -(m * yb.y);
+                    F.y = m * yb.x;
+                    combine(i, F);
+                }
             }
             __syncthreads();
         }

@@ -26,6 +26,7 @@
 // y faces only where the slab holds them, outputs of the first / last wsend rows also go to the
 // neighbours (store_out).  Every value follows the DAG of DESIGN.md §3.1 (bitwise = oracle).
 #pragma once
+#include <algorithm>
 #include <utility>
 #include "generic.cuh"
 
@@ -395,13 +396,30 @@ template <typename T, int ORDER, int BC, int STAGE>
 #ifndef NLSE_S2_MINB
 #define NLSE_S2_MINB (16 / NLSE_S2_WARPS)     // 16 resident warps per SM (<= 128 registers)
 #endif
-__global__ void __launch_bounds__(S2_NT, NLSE_S2_MINB) stage2d_strip(const __grid_constant__ StageArgs<T> A, int nstrips, int rows) {
+__global__ void __launch_bounds__(S2_NT, NLSE_S2_MINB) stage2d_strip(const __grid_constant__ StageArgs<T> A, int nstrips, int rows,
+                                                                     int rows_e) {
+    // items: the interior strips 1 .. nstrips - 2 in chunks of `rows` rows, then the two edge strips
+    // (x faces: the face arithmetic makes a row ~1.6x as long) in shorter chunks of `rows_e` rows, so
+    // that edge warps end with the others (a single wave otherwise waits for them: ncu showed the
+    // SMs active only 57 % of the launch with equal chunks)
     const int item = int(blockIdx.x) * S2_WARPS + int(threadIdx.x >> 5);
-    const int chunk = item / nstrips, s = item - chunk * nstrips;
     const int r_lo = A.g.zf_lo ? 1 : 0, r_hi = A.g.zf_hi ? int(A.g.ny) - 1 : int(A.g.ny);  // rows computed
-    const int ys = r_lo + chunk * rows;                     // (face rows ride along with rows 1, ny - 2)
+    const int ni = nstrips > 2 ? nstrips - 2 : 0;
+    const int nch = (r_hi - r_lo + rows - 1) / rows;
+    int s, ys, ye;
+    if (item < ni * nch) {
+        const int chunk = item / ni;
+        s = 1 + (item - chunk * ni);
+        ys = r_lo + chunk * rows;                          // (face rows ride along with rows 1, ny - 2)
+        ye = min(ys + rows, r_hi);
+    } else {
+        const int ne = nstrips > 1 ? 2 : 1, e = item - ni * nch;
+        const int chunk = e / ne;
+        s = (e - chunk * ne) == 0 ? 0 : nstrips - 1;
+        ys = r_lo + chunk * rows_e;
+        ye = min(ys + rows_e, r_hi);
+    }
     if (ys >= r_hi) return;                                  // (whole warp: no CTA-wide sync here)
-    const int ye = min(ys + rows, r_hi);
     if (s == 0 || s == nstrips - 1) s2_strip<T, ORDER, BC, STAGE, true>(A, s, ys, ye);
     else s2_strip<T, ORDER, BC, STAGE, false>(A, s, ys, ye);
 }
@@ -428,12 +446,18 @@ void launch_strip2d(const StageArgs<T> &A, int nsm, cudaStream_t st) {
         rows = (nrows + nch - 1) / nch;
         if (rows > 32) rows = 32;
     }
-    const int64_t nchunks = (nrows + rows - 1) / rows;
-    const int64_t items = nstrips * nchunks;
+    // edge-strip chunks of rows / div rows: div = 8 measured best (1024^2: 56.2 us/step vs 68.7 at
+    // div 2 and 69.5 at 1; 4096^2 flat, r02 s2d_h / s2d_i)
+    const char *ediv = getenv("NLSE_STRIP_EDGE_DIV");
+    const int64_t div = ediv ? std::max(1, std::atoi(ediv)) : 8;
+    const int64_t rows_e = std::max<int64_t>(1, (rows + div - 1) / div);
+    const int64_t nchunks = (nrows + rows - 1) / rows, nchunks_e = (nrows + rows_e - 1) / rows_e;
+    const int64_t items = (nstrips > 2 ? nstrips - 2 : 0) * nchunks + (nstrips > 1 ? 2 : 1) * nchunks_e;
     auto kern = stage2d_strip<T, ORDER, BC, STAGE>;
     if (S2Slot<T>::SMEM > 48 * 1024)      // (idempotent, per device of the calling thread)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S2Slot<T>::SMEM);
-    kern<<<unsigned((items + S2_WARPS - 1) / S2_WARPS), S2_NT, S2Slot<T>::SMEM, st>>>(A, int(nstrips), int(rows));
+    kern<<<unsigned((items + S2_WARPS - 1) / S2_WARPS), S2_NT, S2Slot<T>::SMEM, st>>>(A, int(nstrips), int(rows),
+                                                                                       int(rows_e));
 }
 
 }  // namespace nlse

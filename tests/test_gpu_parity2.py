@@ -35,7 +35,8 @@ VARIANT_ENV = {
 @pytest.mark.parametrize("kernel", list(VARIANT_ENV))
 @pytest.mark.parametrize("withV", [False, True], ids=["V0", "V"])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-@pytest.mark.parametrize("dims", [(1029,), (6001,), (133, 70), (70, 37, 29)], ids=["1d", "1d_tiled", "2d", "3d"])
+@pytest.mark.parametrize("dims", [(1029,), (3001,), (8001,), (133, 70), (70, 37, 29)],
+                         ids=["1d", "1d_3pts_per_thread", "1d_tiled", "2d", "3d"])
 def test_msd_eps_guard_bitwise(dims, precision, withV, kernel, monkeypatch):
     """R-MSD-GUARD on the GPU: Psi_b' = 0 and eps/2 (guard taken) at face, edge and corner
     neighbours (tests/helpers.guard_points); every kernel path that forms an MSD
@@ -62,7 +63,7 @@ def test_msd_eps_guard_bitwise(dims, precision, withV, kernel, monkeypatch):
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
-@pytest.mark.parametrize("n", [6001, 100001])
+@pytest.mark.parametrize("n", [8001, 100001])
 def test_1d_large_grids_bitwise(n, scheme, bc, precision):
     """1D grids above the persistent single-CTA limit (the paper's Table 1 runs 1D to 3e6 points,
     P:664-686) take the tiled 1D stage kernels: bit for bit against the oracle, with a V array."""
@@ -76,6 +77,25 @@ def test_1d_large_grids_bitwise(n, scheme, bc, precision):
     got, info = run_gpu(dims, h, psi0, k, 9, with_info=True, **kw)
     assert info["variant"] != "rk4_1d_persistent", info
     assert_parity(got, ref, precision, what=f"1D n={n} {scheme} {bc} {precision} {info['variant']}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("n", [3, 4, 5, 1023, 1024, 1025, 2049, 3001])
+def test_1d_persistent_sizes_bitwise(n, scheme, bc, precision):
+    """The persistent single-CTA 1D kernel (one block phase per stage since round 2: D at a point's
+    neighbours and F at b' recomputed by the thread) from 3 points to 3 points per thread."""
+    dims = (n,)
+    h = 0.05
+    psi0 = case_input(dims, seed=n % 991)
+    V = 0.3 * np.abs(inputs.random_smooth(dims, seed=12))
+    kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
+    k = _k(1, h, scheme)
+    ref = run_oracle(dims, h, psi0, k, 23, **kw)
+    got, info = run_gpu(dims, h, psi0, k, 23, with_info=True, **kw)
+    assert info["variant"] == "rk4_1d_persistent", info
+    assert_parity(got, ref, precision, what=f"1D n={n} {scheme} {bc} {precision}")
 
 
 @pytest.mark.parametrize("ndim,precision,chunk", [(3, "fp64", 20), (3, "fp32", 3), (1, "fp64", 7), (2, "fp32", 5),

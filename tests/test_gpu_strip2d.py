@@ -24,7 +24,7 @@ def _k(h, scheme):
     return 0.5 * h * h / (2 * math.sqrt(2)) * (0.75 if scheme == "2shoc" else 1.0)
 
 
-NX = [3, 4, 5, 29, 30, 31, 32, 33, 58, 59, 60, 61, 62, 87]
+NX = [3, 4, 5, 29, 30, 31, 32, 33, 58, 59, 60, 61, 62, 87, 90]
 
 
 @pytest.mark.parametrize("nx", NX)
@@ -42,13 +42,16 @@ def test_strip_widths(nx, bc, scheme):
     assert_parity(got, ref, "fp64", what=f"nx={nx} {scheme} {bc}")
 
 
+@pytest.mark.parametrize("div", ["1", "2", "3"])
 @pytest.mark.parametrize("rows", ["1", "2", "3", "0"])
 @pytest.mark.parametrize("ny", [3, 4, 5, 8, 37])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
-def test_strip_row_chunks(rows, ny, bc, scheme, monkeypatch):
+def test_strip_row_chunks(rows, ny, bc, scheme, div, monkeypatch):
+    """Row chunks of the interior strips (NLSE_STRIP_ROWS) and of the two edge strips (rows / div)."""
     if rows != "0":
         monkeypatch.setenv("NLSE_STRIP_ROWS", rows)
+    monkeypatch.setenv("NLSE_STRIP_EDGE_DIV", div)
     dims = (61, ny)
     h = 0.3
     psi0 = case_input(dims, seed=500 + ny)
