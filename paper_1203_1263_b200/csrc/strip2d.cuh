@@ -1,9 +1,11 @@
 // strip2d.cuh -- 2D stage kernel, round 2 (§8(a) rows a1-a7 for 2D grids, boundary included):
-// one WARP streams a 32-column strip along y, with no shared memory and no CTA barrier.
+// one WARP (one warp per CTA) streams a 32-column strip along y, with no CTA barrier; the only
+// shared memory is the warp's own cp.async staging ring.
 //
-// The 2D configurations (configs[2]: 1024^2 fp64 + V, 75 MB) are L2-resident; the shared-tile
-// kernel (tile2d.cuh: load tile -> barrier -> D tile -> barrier -> combine, one tile per CTA) is
-// latency-bound there (23 us per stage at 1024^2, r02s) and needs a separate boundary kernel.
+// The shared-tile kernel of round 1 (tile2d.cuh: load tile -> barrier -> D tile -> barrier ->
+// combine, one tile per CTA, plus a boundary kernel) was latency-bound on configs[2] (1024^2
+// fp64 + V: 23 us per stage, r02s).  (That grid's 72 MB of state does not make it L2-bound: on
+// B200 the L2 delivers about the HBM rate at that size, profiles/r02_l2_bandwidth.json.)
 // Here the 2.5D z-streaming design of stage3d_tma is taken one dimension down, where a "plane"
 // is one row of a strip, so that a warp alone holds everything it needs:
 //   * lane l holds column gx = xs + l, xs = 1 + s W - H (H = w: 1 CD, 2 2SHOC); lanes
@@ -13,14 +15,16 @@
 //     of rows y - 1, y, y + 1), exactly as the z queues of the 3D kernel;
 //   * the loads of a row (Y two rows ahead, Psi / K_tot / V of the row) are staged S2_NSL - 1 rows
 //     ahead by cp.async into a per-warp shared-memory ring (each lane its own column);
+//   * the two edge strips (x faces: the face arithmetic makes their rows ~1.6x as long) run in
+//     row chunks 8x shorter than the interior strips, so the single wave does not wait for them;
 //   * per row y: D(y + 1) (2SHOC step 1, (2d2shocs1) P:202-210; faces: the Laplacian form of
 //     the BC, (BCDlap) P:320-323, (BCMSDlap) P:336-344, (BCL0lap) P:352-355), step 2 at row y
 //     ((2d2shocs2) P:214-228), F (fsplit) P:424-428 and the RK4 stage combine (RK4_GPU)
 //     P:495-519; CD: L = D;
 //   * the domain boundary is finished in the same pass: the x-face points x = 0 / nx - 1 by the
 //     lane next to the strip's first / last output lane (F(b'), Y(b') by a shuffle from the
-//     inward lane), the y-face rows 0 / ny - 1 in the iterations of rows 1 / ny - 2 (F(b'), Y(b')
-//     of the inward row in registers; corners take b' = (clamp x, clamp y), R-MSD-NBR):
+//     inward lane), the y-face rows 0 / ny - 1 after the row loop from F(b'), Y(b') of rows 1 /
+//     ny - 2 kept in registers (corners take b' = (clamp x, clamp y), R-MSD-NBR):
 //     (BCDdt) P:315-318, (msd) P:331-335, (BCL0dt) P:347-350.  One launch per stage.
 // y-slab mode (§8(e)): rows [-zghost, 0) and [ny, ny + zghost) are the neighbours' ghost rows,
 // y faces only where the slab holds them, outputs of the first / last wsend rows also go to the
