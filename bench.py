@@ -333,7 +333,7 @@ def main():
 
     # dominant kernel: the interior stage kernel family
     # persistent kernels (one launch per nlse_step call) are timed under their tile kind
-    dom = {"rk4_2d_persistent": "stage2d_tile", "rk4_1d_persistent": "stage1d_tile"}.get(info["variant"], info["variant"])
+    dom = {"rk4_2d_persistent": "stage2d_tile", "rk4_1d_persistent": "stage1d_tile", "rk4_1d_cluster": "stage1d_tile"}.get(info["variant"], info["variant"])
     td = timing[dom]
     avg_launch_ms = td["ms"] / max(td["launches"], 1)
     pts_per_launch = td["points"] / max(td["launches"], 1)

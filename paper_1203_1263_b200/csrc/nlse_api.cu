@@ -253,6 +253,24 @@ bool use_persist1d(const nlse_ctx *c) {
     return c->g.nx <= (int64_t(1) << 30) && need <= size_t(optin);
 }
 
+// 1D persistent kernel on a thread-block cluster: NLSE_1D_CLUSTER=N forces N CTAs (0 / 1: the
+// single-CTA kernel); default 8 CTAs (a portable cluster) for 512 <= n <= 3200 (configs[0] 1025
+// points: 3.8 vs 4.1 us/step, 1001-point MSD 5.4 vs 5.7; at 10^4 points the tiled kernels are
+// faster, 9.2 vs 10.4 us/step, r02 c1d2), when every segment holds >= 4 points and fits the CTA.
+int choose_cluster1d(const nlse_ctx *c) {
+    if (c->ndim != 1 || c->interior_kind == KK_GENERIC || c->dist) return 0;
+    const int64_t n = c->g.nx;
+    const char *e = getenv("NLSE_1D_CLUSTER");
+    int64_t nc = e ? std::atoll(e) : ((n >= 512 && n <= 3200) ? 8 : 0);
+    if (nc > 8) nc = 8;
+    if (nc < 2 || n < 4 * nc) return 0;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const size_t need = c->prec == NLSE_FP64 ? cluster1d_smem<double>(int(n), int(nc), c->hasV)
+                                             : cluster1d_smem<float>(int(n), int(nc), c->hasV);
+    return need <= size_t(optin) ? int(nc) : 0;
+}
+
 void drop_graph(nlse_ctx *c) {
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     c->graph_exec = nullptr;
@@ -667,7 +685,8 @@ nlse_status create_common(int ndim, const int64_t dims[3], double h, double a, d
         }
     }
 #undef CREATE_TRY
-    c->persist1d = use_persist1d(c);
+    c->cluster1d = choose_cluster1d(c);
+    c->persist1d = c->cluster1d > 1 || use_persist1d(c);
     c->connected = !dist;
     *out = c;
     return NLSE_OK;
@@ -1094,7 +1113,7 @@ nlse_status nlse_get_info(nlse_ctx *c, nlse_info *out) {
     out->device_bytes = c->device_bytes;
     out->elem_bytes = c->eb;
     snprintf(out->variant, sizeof out->variant, "%s",
-             c->persist1d ? "rk4_1d_persistent"
+             c->persist1d ? (c->cluster1d > 1 ? "rk4_1d_cluster" : "rk4_1d_persistent")
                           : (c->persist2d ? "rk4_2d_persistent"
                                           : (c->fused ? kKindName[KK_FUSED3D] : kKindName[c->interior_kind])));
     out->rank = c->rank;

@@ -123,6 +123,7 @@ struct nlse_ctx {
     bool ghost_stale = false;
     bool virtual_group = false;      // connected by nlse_dist_connect_local: _group calls only
     bool persist1d = false;          // 1D: one persistent CTA per nlse_step call
+    int cluster1d = 0;               // ... or a cluster of this many CTAs (> 1; rk4_1d_cluster)
     bool persist2d = false;          // 2D L2-scale grids: one cooperative launch per nlse_step call
     unsigned *d_bar = nullptr;       // its grid barrier (count, generation)
 };

@@ -4,6 +4,7 @@
 // NLSE_DEFINE_STAGES(_BC), the enqueue entry points of one (precision, dimension, order)
 // family for one or all three BCs (declared in runtime.cuh, called by nlse_api.cu).
 #pragma once
+#include <algorithm>
 #include "runtime.cuh"
 #include "generic.cuh"
 #include "persist1d.cuh"
@@ -232,6 +233,35 @@ void launch_persist1d(nlse_ctx *c, double k, int64_t nsteps) {
         attr.set(c->device, 1);
     }
     LaunchTimer lt(c, KK_TILE1D, c->g.n * nsteps);
+    if (c->cluster1d > 1) {
+        // thread-block cluster of c->cluster1d CTAs, one grid segment each (rk4_1d_cluster)
+        const int nc = c->cluster1d;
+        const int m = (P.n + nc - 1) / nc;
+        const int nt = std::min(1024, (m + 31) / 32 * 32);
+        const size_t csm = cluster1d_smem<T>(P.n, nc, c->hasV);
+        auto kern = rk4_1d_cluster<T, ORDER, BC>;
+        static PerDevice cattr;
+        if (!cattr.get(c->device)) {
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+            cattr.set(c->device, 1);
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(nc), 1, 1);
+        cfg.blockDim = dim3(unsigned(nt), 1, 1);
+        cfg.dynamicSmemBytes = csm;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = unsigned(nc);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, P);
+        return;
+    }
     rk4_1d_persistent<T, ORDER, BC><<<1, P1_THREADS, smem, c->stream>>>(P);
 }
 

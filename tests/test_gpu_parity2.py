@@ -64,9 +64,11 @@ def test_msd_eps_guard_bitwise(dims, precision, withV, kernel, monkeypatch):
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
 @pytest.mark.parametrize("n", [8001, 100001])
-def test_1d_large_grids_bitwise(n, scheme, bc, precision):
+def test_1d_large_grids_bitwise(n, scheme, bc, precision, monkeypatch):
     """1D grids above the persistent single-CTA limit (the paper's Table 1 runs 1D to 3e6 points,
-    P:664-686) take the tiled 1D stage kernels: bit for bit against the oracle, with a V array."""
+    P:664-686) take the tiled 1D stage kernels (NLSE_1D_CLUSTER=0: not the cluster kernel, which
+    holds up to ~25K points): bit for bit against the oracle, with a V array."""
+    monkeypatch.setenv("NLSE_1D_CLUSTER", "0")
     dims = (n,)
     h = 0.05
     psi0 = case_input(dims, seed=n % 997)
@@ -82,10 +84,18 @@ def test_1d_large_grids_bitwise(n, scheme, bc, precision):
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("bc", ["dirichlet", "msd", "l0"])
 @pytest.mark.parametrize("scheme", ["cd", "2shoc"])
-@pytest.mark.parametrize("n", [3, 4, 5, 1023, 1024, 1025, 2049, 3001])
-def test_1d_persistent_sizes_bitwise(n, scheme, bc, precision):
-    """The persistent single-CTA 1D kernel (one block phase per stage since round 2: D at a point's
-    neighbours and F at b' recomputed by the thread) from 3 points to 3 points per thread."""
+@pytest.mark.parametrize("kernel", ["single", "auto", "c2", "c3", "c8"])
+@pytest.mark.parametrize("n", [3, 4, 5, 1023, 1024, 1025, 2049, 3001, 10001])
+def test_1d_persistent_sizes_bitwise(n, scheme, bc, precision, kernel, monkeypatch):
+    """The persistent 1D kernels: one CTA (one block phase per stage since round 2: D at a point's
+    neighbours and F at b' recomputed by the thread), from 3 points to 3 points per thread; and the
+    thread-block-cluster variant (segments of the grid in 2-8 CTAs, neighbours' points through
+    distributed shared memory, a cluster barrier per stage)."""
+    env = {"single": "0", "auto": None, "c2": "2", "c3": "3", "c8": "8"}[kernel]
+    if env is not None:
+        monkeypatch.setenv("NLSE_1D_CLUSTER", env)
+    if kernel == "single" and n > 3001:
+        pytest.skip("beyond one CTA's shared memory")
     dims = (n,)
     h = 0.05
     psi0 = case_input(dims, seed=n % 991)
@@ -94,8 +104,11 @@ def test_1d_persistent_sizes_bitwise(n, scheme, bc, precision):
     k = _k(1, h, scheme)
     ref = run_oracle(dims, h, psi0, k, 23, **kw)
     got, info = run_gpu(dims, h, psi0, k, 23, with_info=True, **kw)
-    assert info["variant"] == "rk4_1d_persistent", info
-    assert_parity(got, ref, precision, what=f"1D n={n} {scheme} {bc} {precision}")
+    if kernel == "single":
+        assert info["variant"] == "rk4_1d_persistent", info
+    elif kernel != "auto" and 4 * int(env) <= n <= 3001:   # (a forced cluster whose segments fit)
+        assert info["variant"] == "rk4_1d_cluster", info
+    assert_parity(got, ref, precision, what=f"1D n={n} {scheme} {bc} {precision} {info['variant']}")
 
 
 @pytest.mark.parametrize("ndim,precision,chunk", [(3, "fp64", 20), (3, "fp32", 3), (1, "fp64", 7), (2, "fp32", 5),
