@@ -699,6 +699,7 @@ nlse_status enqueue_steps(nlse_ctx *c, double k, int64_t nsteps) {
         const bool f64 = c->prec == NLSE_FP64, shoc = c->order == NLSE_2SHOC4;
         (f64 ? (shoc ? persist1d_f64_shoc : persist1d_f64_cd) : (shoc ? persist1d_f32_shoc : persist1d_f32_cd))(
             c, k, nsteps);
+        CUDA_TRY(c, cudaGetLastError());               // (e.g. a cluster launch the device refuses)
         enqueue_add_steps(c, nsteps);
         return NLSE_OK;
     }
