@@ -19,6 +19,14 @@ template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 template <typename T> using cplx = typename Vec2<T>::type;
 
+// Programmatic dependent launch (kernels launched with the programmatic-stream-serialization
+// attribute): pdl_trigger lets the next kernel on the stream be scheduled while this one runs (its
+// CTAs then wait in pdl_wait); pdl_wait blocks until the previous kernel on the stream has completed
+// and its memory is visible -- every global access of a kernel comes after it.  Both are no-ops for
+// kernels launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Componentwise helpers: each is exactly one IEEE operation per component.
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { C r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { C r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }

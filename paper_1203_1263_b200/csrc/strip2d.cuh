@@ -423,7 +423,9 @@ __global__ void __launch_bounds__(S2_NT, NLSE_S2_MINB) stage2d_strip(const __gri
         ys = r_lo + chunk * rows_e;
         ye = min(ys + rows_e, r_hi);
     }
+    pdl_trigger();
     if (ys >= r_hi) return;                                  // (whole warp: no CTA-wide sync here)
+    pdl_wait();                                              // (before any global access)
     if (s == 0 || s == nstrips - 1) s2_strip<T, ORDER, BC, STAGE, true>(A, s, ys, ye);
     else s2_strip<T, ORDER, BC, STAGE, false>(A, s, ys, ye);
 }
@@ -460,8 +462,21 @@ void launch_strip2d(const StageArgs<T> &A, int nsm, cudaStream_t st) {
     auto kern = stage2d_strip<T, ORDER, BC, STAGE>;
     if (S2Slot<T>::SMEM > 48 * 1024)      // (idempotent, per device of the calling thread)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S2Slot<T>::SMEM);
-    kern<<<unsigned((items + S2_WARPS - 1) / S2_WARPS), S2_NT, S2Slot<T>::SMEM, st>>>(A, int(nstrips), int(rows),
-                                                                                       int(rows_e));
+    // programmatic dependent launch (NLSE_PDL=0: off): this launch's CTAs may be scheduled while the
+    // previous stage's tail runs and wait in pdl_wait, overlapping one launch's ramp with the other's
+    // tail
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((items + S2_WARPS - 1) / S2_WARPS), 1, 1);
+    cfg.blockDim = dim3(S2_NT, 1, 1);
+    cfg.dynamicSmemBytes = S2Slot<T>::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    const char *epdl = getenv("NLSE_PDL");
+    cfg.attrs = at;
+    cfg.numAttrs = (epdl && epdl[0] == '0') ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, kern, A, int(nstrips), int(rows), int(rows_e));
 }
 
 }  // namespace nlse
