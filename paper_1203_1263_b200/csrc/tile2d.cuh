@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
     constexpr int H = (ORDER == ORDER_2SHOC) ? 2 : 1;
     __shared__ __align__(16) C ys[T1_N + 2 * H];
     __shared__ __align__(16) C ds[(ORDER == ORDER_2SHOC) ? T1_N + 2 : 1];
+    pdl_trigger();                       // (launched with programmatic dependent launch, launch_tile1d)
+    pdl_wait();
     const int64_t nx = A.g.nx;
     const int64_t x0 = int64_t(blockIdx.x) * T1_N;
     const int tid = threadIdx.x;
@@ -413,12 +415,25 @@ __global__ void __launch_bounds__(T1_NT) stage1d_tile(StageArgs<T> A) {
     }
 }
 
+// Programmatic dependent launch (NLSE_PDL=0: off) for grids of at most 148 CTAs: the ~10^4-point
+// grids of the paper's Table 1 are launch-latency bound (10^4 points 9.8 vs 10.8 us/step; at 10^5
+// points, 391 CTAs, it measured slower: 12.9 vs 11.3, r02 pdl_c).
 template <typename T, int ORDER, int BC, int STAGE>
 void launch_tile1d(const StageArgs<T> &A, cudaStream_t st) {
-    if (A.g.nx >= (int64_t(1) << 20))
-        stage1d_tile<T, ORDER, BC, STAGE, 4><<<unsigned((A.g.nx + 4 * T1_NT - 1) / (4 * T1_NT)), T1_NT, 0, st>>>(A);
-    else
-        stage1d_tile<T, ORDER, BC, STAGE, 1><<<unsigned((A.g.nx + T1_NT - 1) / T1_NT), T1_NT, 0, st>>>(A);
+    const bool big = A.g.nx >= (int64_t(1) << 20);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(big ? (A.g.nx + 4 * T1_NT - 1) / (4 * T1_NT) : (A.g.nx + T1_NT - 1) / T1_NT), 1, 1);
+    cfg.blockDim = dim3(T1_NT, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    const char *e = getenv("NLSE_PDL");
+    cfg.attrs = at;
+    cfg.numAttrs = ((e && e[0] == '0') || cfg.gridDim.x > 148) ? 0 : 1;
+    if (big) cudaLaunchKernelEx(&cfg, stage1d_tile<T, ORDER, BC, STAGE, 4>, A);
+    else cudaLaunchKernelEx(&cfg, stage1d_tile<T, ORDER, BC, STAGE, 1>, A);
 }
 
 }  // namespace nlse
