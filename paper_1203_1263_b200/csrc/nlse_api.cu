@@ -254,14 +254,15 @@ bool use_persist1d(const nlse_ctx *c) {
 }
 
 // 1D persistent kernel on a thread-block cluster: NLSE_1D_CLUSTER=N forces N CTAs (0 / 1: the
-// single-CTA kernel); default 8 CTAs (a portable cluster) for 512 <= n <= 3200 (configs[0] 1025
+// single-CTA kernel); default 8 CTAs (a portable cluster) for fp64 and 512 <= n <= 3200 (configs[0] 1025
 // points: 3.8 vs 4.1 us/step, 1001-point MSD 5.4 vs 5.7; at 10^4 points the tiled kernels are
 // faster, 9.2 vs 10.4 us/step, r02 c1d2), when every segment holds >= 4 points and fits the CTA.
 int choose_cluster1d(const nlse_ctx *c) {
     if (c->ndim != 1 || c->interior_kind == KK_GENERIC || c->dist) return 0;
     const int64_t n = c->g.nx;
     const char *e = getenv("NLSE_1D_CLUSTER");
-    int64_t nc = e ? std::atoll(e) : ((n >= 512 && n <= 3200) ? 8 : 0);
+    // (fp32: the single CTA is faster -- configs[1] fp32 3.87 vs 4.83 us/step, r02fin2 / r02fin3)
+    int64_t nc = e ? std::atoll(e) : ((c->prec == NLSE_FP64 && n >= 512 && n <= 3200) ? 8 : 0);
     if (nc > 8) nc = 8;
     if (nc < 2 || n < 4 * nc) return 0;
     int optin = 0;

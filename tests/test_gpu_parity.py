@@ -62,7 +62,8 @@ def test_matrix_bitwise(ndim, scheme, bc, precision, withV, kernel, monkeypatch)
     kw = dict(a=0.9, s=-1.1, V=V, bc=bc, scheme=scheme, precision=precision)
     ref = run_oracle(dims, h, psi0, k, n, **kw)
     got, info = run_gpu(dims, h, psi0, k, n, generic=generic, with_info=True, **kw)
-    want = {"fast": {1: "rk4_1d_cluster", 2: "stage2d_strip", 3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
+    want = {"fast": {1: "rk4_1d_cluster" if precision == "fp64" else "rk4_1d_persistent", 2: "stage2d_strip",
+                     3: "stage3d_tma"}[ndim], "v1": "stage3d_stream",
             "tile2d": "stage2d_tile", "edge_off": "stage3d_tma",
             "edge_lean": "stage3d_tma", "edge_pp": "stage3d_tma", "msd_recompute": "stage3d_tma", "xfuse_off": "stage3d_tma", "xfuse_on": "stage3d_tma",
             "generic": "stage_generic"}[kernel]
