@@ -143,6 +143,56 @@ def _inward(arr, dims):
     return arr[tuple(idx)]
 
 
+def _complex_plane_wave(dims, h, kvec, amp):
+    coords = inputs.mesh(dims, h)
+    return amp * np.exp(1j * sum(k * c for k, c in zip(kvec, coords)))
+
+
+@pytest.mark.parametrize("scheme", ["cd", "2shoc"])
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_msd_exact_for_complex_plane_waves(oracle_lib, ndim, scheme):
+    """A complex plane wave A exp(i k.x) has |Psi| = A at every point, the state the MSD condition
+    ((msd) P:331-335) is built to preserve: with a constant V every boundary point -- faces, edges
+    and corners, b' the diagonal inward neighbour -- must evolve like the interior, so the whole
+    right-hand side is F = i (a mu + s A^2 - V0) Psi with mu the scheme's plane-wave symbol (CD:
+    sum_a 2(cos k_a h - 1)/h^2; 2SHOC: times (7/6 - cos(k_a h)/6)).  Closed form,
+    independent of how the oracle writes (msd) / (BCMSDlap): a wrong real/imaginary part, sign,
+    neighbour or a dropped N term breaks it at the boundary."""
+    dims = (11, 9, 8)[:ndim]
+    h = 0.3
+    kvec = (0.7, -1.1, 0.4)[:ndim]
+    amp, a, s, v0 = 1.3, 0.8, -1.2, 0.37
+    psi = _complex_plane_wave(dims, h, kvec, amp)
+    V = np.full(psi.shape, v0)
+    mu = 0.0
+    for k in kvec:
+        cd = 2.0 * (math.cos(k * h) - 1.0) / h ** 2
+        mu += cd if scheme == "cd" else cd * (7.0 / 6.0 - math.cos(k * h) / 6.0)
+    F = oracle.rhs(Problem(dims, h, a=a, s=s, bc="msd", scheme=scheme), psi, V)
+    want = 1j * (a * mu + s * amp ** 2 - v0) * psi
+    np.testing.assert_allclose(F, want, rtol=0, atol=1e-11 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("ndim", [1, 2, 3])
+def test_msd_face_laplacian_on_plane_wave_with_varying_v(oracle_lib, ndim):
+    """(BCMSDlap) P:336-344 on a complex plane wave with a non-constant V: D_b' / Psi_b' is the CD
+    symbol lambda = sum_a 2(cos k_a h - 1)/h^2 at every interior b', so the face value must be
+    D_b = [lambda + (N_b' - N_b)/a] Psi_b with N = s|Psi|^2 - V = s A^2 - V (closed form; pins the
+    sign and the 1/a of the potential term, which a constant V cannot see)."""
+    dims = (11, 9, 8)[:ndim]
+    h = 0.3
+    kvec = (0.7, -1.1, 0.4)[:ndim]
+    amp, a, s = 1.3, 0.8, -1.2
+    psi = _complex_plane_wave(dims, h, kvec, amp)
+    V = 0.3 + 0.2 * np.abs(inputs.random_smooth(dims, seed=41))
+    lam = sum(2.0 * (math.cos(k * h) - 1.0) / h ** 2 for k in kvec)
+    D, _ = oracle.laplacian(Problem(dims, h, a=a, s=s, bc="msd", scheme="2shoc"), psi, V)
+    f = _face_mask(dims)
+    N = s * amp ** 2 - V
+    want = (lam + (_inward(N, dims) - N) / a) * psi
+    np.testing.assert_allclose(D[f], want[f], rtol=0, atol=1e-11 * np.abs(want[f]).max())
+
+
 @pytest.mark.parametrize("ndim", [1, 2, 3])
 def test_dirichlet_laplacian_form_is_consistent(oracle_lib, ndim):
     """(BCDlap) P:320-323 substituted into F = i[a Lap + N]Psi gives dPsi_b/dt = 0 (BCDdt), to a few ulp."""
