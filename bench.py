@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--generic", action="store_true", help="use the one-thread-per-point kernels")
     ap.add_argument("--scheme", default=None, help="override the workload's scheme (cd | 2shoc), for experiments")
     ap.add_argument("--precision", default=None, help="override the workload's precision (fp32 | fp64)")
+    ap.add_argument("--bc", default=None, help="override the workload's boundary condition (dirichlet | msd | l0)")
     return ap.parse_args()
 
 
@@ -290,6 +291,8 @@ def main():
         cfg["scheme"] = args.scheme
     if args.precision:
         cfg["precision"] = args.precision
+    if args.bc:
+        cfg["bc"] = args.bc
     B = bytes_min_per_point(cfg)
     peak, peak_src = measured_peaks()
     npts = int(np.prod(cfg["dims"])) * (world if replicas else 1)   # whole job

@@ -1015,12 +1015,16 @@ __device__ __forceinline__ void t3_fast(const CUtensorMap *mY, const CUtensorMap
 #ifndef NLSE_F32_MINB8
 #define NLSE_F32_MINB8 3
 #endif
-template <typename T, int TYV>
+#ifndef NLSE_F32_MINB8_DIR
+#define NLSE_F32_MINB8_DIR NLSE_F32_MINB8
+#endif
+template <typename T, int TYV, int BC = BC_MSD>
 constexpr int t3_min_blocks() {
-    return TYV == 8 ? (sizeof(T) == 8 ? 2 : NLSE_F32_MINB8) : (sizeof(T) == 8 ? 1 : NLSE_F32_MINB);
+    return TYV == 8 ? (sizeof(T) == 8 ? 2 : (BC == BC_DIRICHLET ? NLSE_F32_MINB8_DIR : NLSE_F32_MINB8))
+                    : (sizeof(T) == 8 ? 1 : NLSE_F32_MINB);
 }
 template <typename T, int ORDER, int BC, int STAGE, int P, int TYV>
-__global__ void __launch_bounds__(32 * TYV, t3_min_blocks<T, TYV>())
+__global__ void __launch_bounds__(32 * TYV, t3_min_blocks<T, TYV, BC>())
 stage3d_tma(const __grid_constant__ CUtensorMap mY, const __grid_constant__ CUtensorMap mP,
             const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
             const __grid_constant__ StageArgs<T> A, int zchunk, int ntx, int nty, int force_edge, int band) {
